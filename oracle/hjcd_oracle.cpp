@@ -1,0 +1,1081 @@
+/*
+ * hjcd_oracle.cpp — fp64 CPU ORACLE for HJCD-IK (arXiv 2510.07514).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or constant generator with the CUDA path
+ * under paper_2510_07514_b200/csrc/; neither side includes the other.
+ *
+ * Written from PAPER.md ("P:NNN" = line of /root/reference/PAPER.md), plainly
+ * and slowly, in fp64, following the paper's algorithms step by step:
+ *   - FK as a literal product of 4x4 homogeneous matrices (Eq. 1);
+ *   - geometric Jacobian columns [z_i x (P_ee - P_i); z_i] (Eq. 7);
+ *   - quaternion error (Eq. 5) and angle-axis form (Eq. 10);
+ *   - CCD projections and angle, literal normalise/project/arccos form
+ *     (Eqs. 8-9);
+ *   - PO-CCD (Alg. 3) scoring every candidate by a FULL FK of
+ *     theta + dtheta*e_j (literal P:222), NOT the rigid-rotation shortcut the
+ *     GPU uses;
+ *   - top-K by stable sort + replication (Alg. 2 l.2-8);
+ *   - PJ-IK (Alg. 4) solving the literal n x n weighted normal
+ *     equations (Eq. 12) by Cholesky, NOT the GPU's 6x6
+ *     push-through form; dogleg (Eqs. 14-15), single-coordinate
+ *     (Eq. 16) and perturbation fallbacks.
+ * Where the paper is silent/garbled the reading is the one recorded in
+ * DESIGN.md "Readings" (R-numbers; the same ids as SURVEY.md §8(c) C1-C35).
+ *
+ * Random numbers: Philox4x32-10 (Random123 definition), counter-based, so both
+ * sides draw the same uniforms (R30).  Uniform -> joint value is
+ * evaluated in fp32 with an explicit fmaf so initial seeds are bitwise equal
+ * (the one place fp32 appears here, by design); Gaussians via fp64 Box-Muller.
+ *
+ * Decision margins: every discrete decision (argmin, gamma test, convergence
+ * test, line-search comparison, ...) records how far it was from flipping.  The
+ * per-seed minimum lets the parity tests tell a genuine bug apart from an
+ * fp32-vs-fp64 near-tie flip.
+ */
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_MAXJ 64
+
+extern "C" {
+
+/* Robot as given by the user: a serial chain, base -> tip (D1).
+ * type: 0 revolute, 1 prismatic, 2 fixed.  Only non-fixed joints are DoF. */
+typedef struct {
+    int32_t n;
+    int32_t type[ORACLE_MAXJ];
+    double origin_xyz[ORACLE_MAXJ][3];
+    double origin_quat[ORACLE_MAXJ][4]; /* w x y z */
+    double axis[ORACLE_MAXJ][3];
+    double lo[ORACLE_MAXJ];
+    double hi[ORACLE_MAXJ];
+    double ee_xyz[3];
+    double ee_quat[4];
+} OracleRobot;
+
+/* Algorithm parameters (Alg. 2-4 headers; defaults in
+ * DESIGN.md R5, R11, R12, R15-R17, R20-R28). */
+typedef struct {
+    int32_t M, K, B;
+    int32_t ccd_iters, lm_iters;
+    double eps_p_coarse, eps_o_coarse;
+    double eps_p_fine, eps_o_fine;
+    double gamma, delta0, delta_rho, delta_min;
+    double sigma_ccd, sigma_rep, sigma_lm;
+    double lambda, d_floor, R, beta;
+    int32_t A;
+    double w_p, w_o;
+    double succ_p, succ_o;
+    double tau_deg;
+    uint64_t rng_seed;
+    int32_t repl_noise_all;
+} OracleConfig;
+
+} /* extern "C" */
+
+namespace {
+
+const double PI = 3.14159265358979323846;
+const double INF = std::numeric_limits<double>::infinity();
+
+/* ---------------- small fp64 linear algebra ---------------- */
+struct V3 { double x, y, z; };
+struct Qt { double w, x, y, z; };
+struct H4 { double m[4][4]; };
+
+V3 v3(double x, double y, double z) { V3 r = {x, y, z}; return r; }
+V3 add(V3 a, V3 b) { return v3(a.x + b.x, a.y + b.y, a.z + b.z); }
+V3 sub(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }
+V3 scl(V3 a, double s) { return v3(a.x * s, a.y * s, a.z * s); }
+double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+V3 cross(V3 a, V3 b) { return v3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x); }
+double norm(V3 a) { return std::sqrt(dot(a, a)); }
+
+H4 h_identity() {
+    H4 h;
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) h.m[i][j] = (i == j) ? 1.0 : 0.0;
+    return h;
+}
+
+H4 h_mul(const H4& a, const H4& b) {
+    H4 c;
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 4; ++k) s += a.m[i][k] * b.m[k][j];
+            c.m[i][j] = s;
+        }
+    return c;
+}
+
+/* rotation matrix of a unit quaternion (w,x,y,z) */
+H4 h_from_pose(const double xyz[3], const double q_in[4]) {
+    double w = q_in[0], x = q_in[1], y = q_in[2], z = q_in[3];
+    double nq = std::sqrt(w * w + x * x + y * y + z * z);
+    w /= nq; x /= nq; y /= nq; z /= nq;
+    H4 h = h_identity();
+    h.m[0][0] = 1 - 2 * (y * y + z * z); h.m[0][1] = 2 * (x * y - w * z);     h.m[0][2] = 2 * (x * z + w * y);
+    h.m[1][0] = 2 * (x * y + w * z);     h.m[1][1] = 1 - 2 * (x * x + z * z); h.m[1][2] = 2 * (y * z - w * x);
+    h.m[2][0] = 2 * (x * z - w * y);     h.m[2][1] = 2 * (y * z + w * x);     h.m[2][2] = 1 - 2 * (x * x + y * y);
+    h.m[0][3] = xyz[0]; h.m[1][3] = xyz[1]; h.m[2][3] = xyz[2];
+    return h;
+}
+
+/* Rodrigues rotation about unit axis a by angle t, as a 4x4 */
+H4 h_rot_axis(V3 a, double t) {
+    double na = norm(a);
+    a = scl(a, 1.0 / na);
+    double c = std::cos(t), s = std::sin(t), C = 1.0 - c;
+    H4 h = h_identity();
+    h.m[0][0] = c + a.x * a.x * C;       h.m[0][1] = a.x * a.y * C - a.z * s; h.m[0][2] = a.x * a.z * C + a.y * s;
+    h.m[1][0] = a.y * a.x * C + a.z * s; h.m[1][1] = c + a.y * a.y * C;       h.m[1][2] = a.y * a.z * C - a.x * s;
+    h.m[2][0] = a.z * a.x * C - a.y * s; h.m[2][1] = a.z * a.y * C + a.x * s; h.m[2][2] = c + a.z * a.z * C;
+    return h;
+}
+
+H4 h_trans_axis(V3 a, double d) {
+    double na = norm(a);
+    H4 h = h_identity();
+    h.m[0][3] = a.x / na * d; h.m[1][3] = a.y / na * d; h.m[2][3] = a.z / na * d;
+    return h;
+}
+
+/* rotation matrix -> unit quaternion (Shepperd), canonical w >= 0 (D2) */
+Qt quat_from_h(const H4& h) {
+    double r00 = h.m[0][0], r11 = h.m[1][1], r22 = h.m[2][2];
+    double tr = r00 + r11 + r22;
+    Qt q;
+    if (tr > 0) {
+        double s = std::sqrt(tr + 1.0) * 2.0;
+        q.w = 0.25 * s;
+        q.x = (h.m[2][1] - h.m[1][2]) / s;
+        q.y = (h.m[0][2] - h.m[2][0]) / s;
+        q.z = (h.m[1][0] - h.m[0][1]) / s;
+    } else if (r00 > r11 && r00 > r22) {
+        double s = std::sqrt(1.0 + r00 - r11 - r22) * 2.0;
+        q.w = (h.m[2][1] - h.m[1][2]) / s;
+        q.x = 0.25 * s;
+        q.y = (h.m[0][1] + h.m[1][0]) / s;
+        q.z = (h.m[0][2] + h.m[2][0]) / s;
+    } else if (r11 > r22) {
+        double s = std::sqrt(1.0 + r11 - r00 - r22) * 2.0;
+        q.w = (h.m[0][2] - h.m[2][0]) / s;
+        q.x = (h.m[0][1] + h.m[1][0]) / s;
+        q.y = 0.25 * s;
+        q.z = (h.m[1][2] + h.m[2][1]) / s;
+    } else {
+        double s = std::sqrt(1.0 + r22 - r00 - r11) * 2.0;
+        q.w = (h.m[1][0] - h.m[0][1]) / s;
+        q.x = (h.m[0][2] + h.m[2][0]) / s;
+        q.y = (h.m[1][2] + h.m[2][1]) / s;
+        q.z = 0.25 * s;
+    }
+    double nq = std::sqrt(q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z);
+    q.w /= nq; q.x /= nq; q.y /= nq; q.z /= nq;
+    if (q.w < 0) { q.w = -q.w; q.x = -q.x; q.y = -q.y; q.z = -q.z; }
+    return q;
+}
+
+/* Hamilton product a (x) b */
+Qt qmul(Qt a, Qt b) {
+    Qt r;
+    r.w = a.w * b.w - a.x * b.x - a.y * b.y - a.z * b.z;
+    r.x = a.w * b.x + a.x * b.w + a.y * b.z - a.z * b.y;
+    r.y = a.w * b.y - a.x * b.z + a.y * b.w + a.z * b.x;
+    r.z = a.w * b.z + a.x * b.y - a.y * b.x + a.z * b.w;
+    return r;
+}
+Qt qconj(Qt a) { Qt r = {a.w, -a.x, -a.y, -a.z}; return r; }
+
+/* ---------------- robot + FK ---------------- */
+struct Robot {
+    const OracleRobot* r;
+    int dof;
+    std::vector<int> dof_entry; /* dof index -> entry in r arrays */
+};
+
+Robot make_robot(const OracleRobot* r) {
+    Robot rb;
+    rb.r = r;
+    rb.dof = 0;
+    for (int i = 0; i < r->n; ++i)
+        if (r->type[i] != 2) { rb.dof_entry.push_back(i); rb.dof++; }
+    return rb;
+}
+
+struct Frames {
+    std::vector<V3> P;  /* P_i: world position of joint i (Eq. 7) */
+    std::vector<V3> z;  /* z_i: world axis of joint i (Eq. 7) */
+    V3 pee;             /* end-effector position */
+    Qt qee;             /* end-effector orientation, w >= 0 */
+};
+
+/* Eq. 1: P_ee = f(theta); literal product
+ * T = Origin_1 * Joint_1(theta_1) * ... * Origin_n * Joint_n(theta_n) * EE. */
+void fk(const Robot& rb, const double* theta, Frames& F) {
+    const OracleRobot* r = rb.r;
+    F.P.assign(rb.dof, v3(0, 0, 0));
+    F.z.assign(rb.dof, v3(0, 0, 0));
+    H4 T = h_identity();
+    int d = 0;
+    for (int i = 0; i < r->n; ++i) {
+        T = h_mul(T, h_from_pose(r->origin_xyz[i], r->origin_quat[i]));
+        if (r->type[i] == 2) continue;
+        V3 a = v3(r->axis[i][0], r->axis[i][1], r->axis[i][2]);
+        a = scl(a, 1.0 / norm(a));
+        if (r->type[i] == 0) T = h_mul(T, h_rot_axis(a, theta[d]));
+        else T = h_mul(T, h_trans_axis(a, theta[d]));
+        F.P[d] = v3(T.m[0][3], T.m[1][3], T.m[2][3]);
+        F.z[d] = v3(T.m[0][0] * a.x + T.m[0][1] * a.y + T.m[0][2] * a.z,
+                    T.m[1][0] * a.x + T.m[1][1] * a.y + T.m[1][2] * a.z,
+                    T.m[2][0] * a.x + T.m[2][1] * a.y + T.m[2][2] * a.z);
+        d++;
+    }
+    T = h_mul(T, h_from_pose(r->ee_xyz, r->ee_quat));
+    F.pee = v3(T.m[0][3], T.m[1][3], T.m[2][3]);
+    F.qee = quat_from_h(T);
+}
+
+/* Eq. 7: J columns [z_i x (P_ee - P_i); z_i] (revolute);
+ * prismatic extension [z_i; 0] (R32).  J row-major 6 x dof. */
+void jacobian(const Robot& rb, const Frames& F, double* J) {
+    int n = rb.dof;
+    for (int d = 0; d < n; ++d) {
+        int e = rb.dof_entry[d];
+        V3 col_p, col_o;
+        if (rb.r->type[e] == 0) {
+            col_p = cross(F.z[d], sub(F.pee, F.P[d]));
+            col_o = F.z[d];
+        } else {
+            col_p = F.z[d];
+            col_o = v3(0, 0, 0);
+        }
+        J[0 * n + d] = col_p.x; J[1 * n + d] = col_p.y; J[2 * n + d] = col_p.z;
+        J[3 * n + d] = col_o.x; J[4 * n + d] = col_o.y; J[5 * n + d] = col_o.z;
+    }
+}
+
+/* Eq. 5: q_err = q_t (x) q_e^-1 = [w, v];
+ * omega = 2 atan2(|v|, |w|)/|v| * v, with q_err canonicalised to w >= 0 first
+ * (R1: the literal |w| with un-flipped v negates omega when w < 0). */
+V3 quat_error(Qt qt, Qt qe) {
+    Qt q = qmul(qt, qconj(qe));
+    if (q.w < 0) { q.w = -q.w; q.x = -q.x; q.y = -q.y; q.z = -q.z; }
+    V3 v = v3(q.x, q.y, q.z);
+    double s = norm(v);
+    if (s < 1e-300) return scl(v, 2.0 / q.w); /* smooth limit 2v/w */
+    return scl(v, 2.0 * std::atan2(s, q.w) / s);
+}
+
+/* Eq. 10: phi = 2 arccos(w), a = v / sin(phi/2), after the w >= 0
+ * canonicalisation (R2).  phi < 1e-9 => caller treats the update as zero. */
+void angle_axis(Qt qt, Qt qe, double* phi, V3* a) {
+    Qt q = qmul(qt, qconj(qe));
+    if (q.w < 0) { q.w = -q.w; q.x = -q.x; q.y = -q.y; q.z = -q.z; }
+    double w = std::min(1.0, q.w);
+    *phi = 2.0 * std::acos(w);
+    double s = std::sin(*phi / 2.0);
+    if (*phi < 1e-9 || s <= 0) { *phi = 0; *a = v3(0, 0, 1); return; }
+    *a = scl(v3(q.x, q.y, q.z), 1.0 / s);
+}
+
+/* ---------------- Philox4x32-10 (Random123), R30 ---------------- */
+void philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    uint32_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+    uint32_t k[2] = {key_in[0], key_in[1]};
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) { k[0] += 0x9E3779B9u; k[1] += 0xBB67AE85u; }
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c[0];
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c[2];
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c[1] ^ k[0];
+        uint32_t n2 = hi0 ^ c[3] ^ k[1];
+        c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+    }
+    out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
+}
+
+enum { P_INIT = 1, P_PERTURB = 2, P_REPL = 3, P_PJPERT = 4 };
+
+/* u = ((x >> 9) + 0.5) * 2^-23: exact in fp32, strictly inside (0, 1) */
+double u01(uint32_t x) { return ((double)(x >> 9) + 0.5) * (1.0 / 8388608.0); }
+
+/* the 4 uniforms of draw block `blk` of stream (tid, sid, purpose, iter) */
+void draw4(uint64_t seed, uint64_t tid, uint32_t sid, uint32_t purpose, uint32_t iter,
+           uint32_t blk, double u[4]) {
+    uint32_t ctr[4] = {(uint32_t)tid, sid, (purpose << 24) | (iter & 0xFFFFFFu), blk};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t o[4];
+    philox4x32_10(ctr, key, o);
+    for (int i = 0; i < 4; ++i) u[i] = u01(o[i]);
+}
+
+/* standard normals for joint d: block d/4, Box-Muller pairs (u0,u1),(u2,u3) */
+double normal_for_joint(uint64_t seed, uint64_t tid, uint32_t sid, uint32_t purpose,
+                        uint32_t iter, int d) {
+    double u[4];
+    draw4(seed, tid, sid, purpose, iter, (uint32_t)(d / 4), u);
+    int e = d % 4;
+    int pair = e / 2;
+    double ua = u[2 * pair], ub = u[2 * pair + 1];
+    double rr = std::sqrt(-2.0 * std::log(ua));
+    return (e % 2 == 0) ? rr * std::cos(2.0 * PI * ub) : rr * std::sin(2.0 * PI * ub);
+}
+
+double clampd(double x, double lo, double hi) { return std::min(std::max(x, lo), hi); }
+
+/* ---------------- target ---------------- */
+struct Target { V3 p; Qt q; bool valid; };
+
+/* S2 / R-target: read fp32 pose, normalise q if | |q| - 1 | <= 1e-3 else invalid */
+Target read_target(const float* t7) {
+    Target t;
+    t.p = v3(t7[0], t7[1], t7[2]);
+    double w = t7[3], x = t7[4], y = t7[5], z = t7[6];
+    double nq = std::sqrt(w * w + x * x + y * y + z * z);
+    t.valid = std::fabs(nq - 1.0) <= 1e-3 && std::isfinite(nq) &&
+              std::isfinite(t.p.x) && std::isfinite(t.p.y) && std::isfinite(t.p.z);
+    if (!(nq > 0)) nq = 1;
+    t.q.w = w / nq; t.q.x = x / nq; t.q.y = y / nq; t.q.z = z / nq;
+    if (t.q.w < 0) { t.q.w = -t.q.w; t.q.x = -t.q.x; t.q.y = -t.q.y; t.q.z = -t.q.z; }
+    return t;
+}
+
+struct Err { double ep, eo; V3 rp, om; };
+
+/* Eq. 4: r = [P_t - P_ee, omega] */
+Err residual(const Frames& F, const Target& t) {
+    Err e;
+    e.rp = sub(t.p, F.pee);
+    e.om = quat_error(t.q, F.qee);
+    e.ep = norm(e.rp);
+    e.eo = norm(e.om);
+    return e;
+}
+
+/* margins of boolean combinations of threshold tests (see header) */
+double margin_and(bool a, double ma, bool b, double mb) {
+    if (a && b) return std::min(ma, mb);
+    if (a && !b) return mb;
+    if (!a && b) return ma;
+    return std::max(ma, mb);
+}
+double margin_or(bool a, double ma, bool b, double mb) {
+    if (a && b) return std::max(ma, mb);
+    if (a && !b) return ma;
+    if (!a && b) return mb;
+    return std::min(ma, mb);
+}
+
+/* ---------------- CCD steps ---------------- */
+/* Eqs. 8-9, literal: normalise, project onto the plane of r_j,
+ * arccos of the normalised projections (magnitude) with the sign of the triple
+ * product z.(u_proj x v_proj) (R3).  Degenerate projection (R4): the raw
+ * projections |P_ee - P_j|_perp or |P_t - P_j|_perp below tau_deg => 0.
+ * Also returns the distance of the degeneracy tests from tau (margin). */
+double ccd_position_step(V3 Pj, V3 rj, V3 pee, V3 pt, double tau, double* margin) {
+    V3 uraw = sub(pee, Pj), vraw = sub(pt, Pj);
+    double rr = dot(rj, rj);
+    V3 uraw_p = sub(uraw, scl(rj, dot(uraw, rj) / rr));
+    V3 vraw_p = sub(vraw, scl(rj, dot(vraw, rj) / rr));
+    double nu = norm(uraw_p), nv = norm(vraw_p);
+    /* a projection norm within a decade of tau is a live decision; far from it
+     * (e.g. the ee exactly on the axis, nu ~ 1e-17) it is structural */
+    if (margin) {
+        *margin = INF;
+        if (nu > 0.1 * tau && nu < 10 * tau) *margin = std::fabs(nu - tau);
+        if (nv > 0.1 * tau && nv < 10 * tau) *margin = std::min(*margin, std::fabs(nv - tau));
+    }
+    if (nu < tau || nv < tau) return 0.0;
+    V3 u = scl(uraw, 1.0 / norm(uraw));
+    V3 v = scl(vraw, 1.0 / norm(vraw));
+    V3 ur = scl(rj, dot(u, rj) / rr);
+    V3 vr = scl(rj, dot(v, rj) / rr);
+    V3 up = sub(u, ur), vp = sub(v, vr);
+    double c = dot(scl(vp, 1.0 / norm(vp)), scl(up, 1.0 / norm(up)));
+    double mag = std::acos(clampd(c, -1.0, 1.0));
+    double sgn = dot(rj, cross(up, vp));
+    return (sgn > 0) ? mag : (sgn < 0 ? -mag : 0.0);
+}
+
+/* delta(k) = max(delta_min, delta0 * rho^k) (R5) */
+double delta_k(const OracleConfig& c, int k) {
+    return std::max(c.delta_min, c.delta0 * std::pow(c.delta_rho, (double)k));
+}
+
+/* Eq. 11: dtheta = delta(k) sgn(a . r_j) phi, sgn(0) = 0 */
+double ccd_orientation_step(double phi, V3 a, V3 rj, double dk) {
+    if (phi <= 0) return 0.0;
+    double s = dot(a, rj);
+    double sg = (s > 0) ? 1.0 : (s < 0 ? -1.0 : 0.0);
+    return dk * sg * phi;
+}
+
+/* ---------------- PO-CCD one seed (Alg. 3) ---------------- */
+struct SeedOut { double ep, eo; int iters; double margin; };
+
+SeedOut po_ccd_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
+                    uint32_t sid, std::vector<double>& th) {
+    const OracleRobot* r = rb.r;
+    int n = rb.dof;
+    SeedOut so;
+    so.margin = INF;
+    Frames F, Fc;
+    std::vector<double> thc(n), thh(n);
+    int k = 0;
+    Err e;
+    for (k = 0;; ++k) {
+        fk(rb, th.data(), F);
+        e = residual(F, tgt);
+        /* Alg. 3 l.14, unsquared reading R12; checked at iteration
+         * start so a seed on the answer stops with 0 updates */
+        bool cp = e.ep < c.eps_p_coarse, co = e.eo < c.eps_o_coarse;
+        so.margin = std::min(so.margin, margin_and(cp, std::fabs(e.ep - c.eps_p_coarse), co,
+                                                   std::fabs(e.eo - c.eps_o_coarse)));
+        if (cp && co) break;
+        if (k == c.ccd_iters) break;
+
+        double phi; V3 ahat;
+        angle_axis(tgt.q, F.qee, &phi, &ahat);
+        double dk = delta_k(c, k);
+        std::vector<double> sp(n), sop(n), dp(n), dor(n);
+        for (int j = 0; j < n; ++j) {
+            int ent = rb.dof_entry[j];
+            double lo = r->lo[ent], hi = r->hi[ent];
+            /* position candidate (Eqs. 8-9); prismatic: z.(P_t - P_ee) (R32) */
+            double stepp;
+            if (r->type[ent] == 0) {
+                double mdeg;
+                stepp = ccd_position_step(F.P[j], F.z[j], F.pee, tgt.p, c.tau_deg, &mdeg);
+                so.margin = std::min(so.margin, mdeg);
+            } else {
+                stepp = dot(F.z[j], sub(tgt.p, F.pee));
+            }
+            /* joint limits on candidates (R7) */
+            dp[j] = clampd(th[j] + stepp, lo, hi) - th[j];
+            thc = th; thc[j] = th[j] + dp[j];
+            fk(rb, thc.data(), Fc);                     /* literal P:222: full FK */
+            sp[j] = norm(sub(tgt.p, Fc.pee));
+            /* orientation candidate (Eqs. 10-11); prismatic: 0 */
+            double stepo = 0.0;
+            if (r->type[ent] == 0) {
+                stepo = ccd_orientation_step(phi, ahat, F.z[j], dk);
+                if (phi > 0) so.margin = std::min(so.margin, std::fabs(dot(ahat, F.z[j])));
+            }
+            dor[j] = clampd(th[j] + stepo, lo, hi) - th[j];
+            thc = th; thc[j] = th[j] + dor[j];
+            fk(rb, thc.data(), Fc);
+            sop[j] = norm(quat_error(tgt.q, Fc.qee));
+        }
+        /* Alg. 3 l.9: argmin over joints, ties -> lower index (R6) */
+        int jp = 0, jo = 0;
+        for (int j = 1; j < n; ++j) {
+            if (sp[j] < sp[jp]) jp = j;
+            if (sop[j] < sop[jo]) jo = j;
+        }
+        for (int j = 0; j < n; ++j) {
+            /* distance to the nearest competitor with a different outcome */
+            if (j != jp && (dp[j] != 0.0 || dp[jp] != 0.0))
+                so.margin = std::min(so.margin, std::fabs(sp[j] - sp[jp]));
+            if (j != jo && (dor[j] != 0.0 || dor[jo] != 0.0))
+                so.margin = std::min(so.margin, std::fabs(sop[j] - sop[jo]));
+        }
+        /* Alg. 3 l.10 + P:201: same joint -> larger |dtheta|, tie -> position (R8) */
+        thh = th;
+        if (jp == jo) {
+            if (dp[jp] != dor[jo]) /* equal steps = same outcome, no decision */
+                so.margin = std::min(so.margin, std::fabs(std::fabs(dp[jp]) - std::fabs(dor[jo])));
+            if (std::fabs(dp[jp]) >= std::fabs(dor[jo])) thh[jp] = th[jp] + dp[jp];
+            else thh[jo] = th[jo] + dor[jo];
+        } else {
+            thh[jp] = th[jp] + dp[jp];
+            thh[jo] = th[jo] + dor[jo];
+        }
+        fk(rb, thh.data(), Fc);
+        Err eh = residual(Fc, tgt);
+        /* Alg. 3 l.11 read as an improvement test on either space (R10) */
+        double ip = e.ep - eh.ep, io = e.eo - eh.eo;
+        bool ap = ip > c.gamma, ao = io > c.gamma;
+        so.margin = std::min(so.margin, margin_or(ap, std::fabs(ip - c.gamma), ao,
+                                                  std::fabs(io - c.gamma)));
+        if (ap || ao) {
+            th = thh;
+        } else {
+            /* Alg. 3 l.13: theta + N(0, sigma_ccd^2 I), clamp (R11) */
+            for (int j = 0; j < n; ++j) {
+                int ent = rb.dof_entry[j];
+                double g = normal_for_joint(c.rng_seed, tid, sid, P_PERTURB, (uint32_t)k, j);
+                th[j] = clampd(th[j] + c.sigma_ccd * g, r->lo[ent], r->hi[ent]);
+            }
+        }
+    }
+    so.ep = e.ep;
+    so.eo = e.eo;
+    so.iters = k;
+    return so;
+}
+
+/* uniform seed in limits (Alg. 3 l.2-3), fp32 fmaf on purpose (R30) */
+void uniform_seed(const Robot& rb, uint64_t seed, uint64_t tid, uint32_t sid, double* th) {
+    for (int j = 0; j < rb.dof; ++j) {
+        int ent = rb.dof_entry[j];
+        double u[4];
+        draw4(seed, tid, sid, P_INIT, 0, (uint32_t)(j / 4), u);
+        float lo = (float)rb.r->lo[ent], hi = (float)rb.r->hi[ent];
+        float uf = (float)u[j % 4];
+        th[j] = (double)std::fmaf(hi - lo, uf, lo);
+    }
+}
+
+/* ---------------- dense SPD solve (Cholesky), n x n ---------------- */
+bool cholesky_solve(std::vector<double> A, int n, const double* b, double* x) {
+    /* A = L L^T in place (lower) */
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j <= i; ++j) {
+            double s = A[i * n + j];
+            for (int k = 0; k < j; ++k) s -= A[i * n + k] * A[j * n + k];
+            if (i == j) {
+                if (!(s > 0)) return false;
+                A[i * n + i] = std::sqrt(s);
+            } else {
+                A[i * n + j] = s / A[j * n + j];
+            }
+        }
+    }
+    std::vector<double> y(n);
+    for (int i = 0; i < n; ++i) {
+        double s = b[i];
+        for (int k = 0; k < i; ++k) s -= A[i * n + k] * y[k];
+        y[i] = s / A[i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        double s = y[i];
+        for (int k = i + 1; k < n; ++k) s -= A[k * n + i] * x[k];
+        x[i] = s / A[i * n + i];
+    }
+    return true;
+}
+
+/* ---------------- PJ-IK pieces (Alg. 4) ---------------- */
+/* rho = -r = [P_ee - P_t; -omega] (R19), 6-vector */
+void rho_of(const Err& e, double rho[6]) {
+    rho[0] = -e.rp.x; rho[1] = -e.rp.y; rho[2] = -e.rp.z;
+    rho[3] = -e.om.x; rho[4] = -e.om.y; rho[5] = -e.om.z;
+}
+
+/* W (R17): diag(w_p I3, w_o I3) * diag(1 / (1 + |J_row_i|)) */
+void weights(const OracleConfig& c, const double* J, int n, double W[6]) {
+    for (int i = 0; i < 6; ++i) {
+        double s = 0;
+        for (int j = 0; j < n; ++j) s += J[i * n + j] * J[i * n + j];
+        W[i] = (i < 3 ? c.w_p : c.w_o) / (1.0 + std::sqrt(s));
+    }
+}
+
+double cost_w(const double W[6], const double rho[6]) {
+    double s = 0;
+    for (int i = 0; i < 6; ++i) s += (W[i] * rho[i]) * (W[i] * rho[i]);
+    return 0.5 * s;
+}
+
+double norm6(const double v[6]) {
+    double s = 0;
+    for (int i = 0; i < 6; ++i) s += v[i] * v[i];
+    return std::sqrt(s);
+}
+
+/* Eq. 12 with the missing W restored (R18), D = max(diag(J^T J),
+ * d_floor) (R20): (J^T W^2 J + lambda D) dtheta = -J^T W^2 rho, literal n x n. */
+bool lm_step(const OracleConfig& c, const double* J, int n, const double W[6],
+             const double rho[6], double* dth) {
+    std::vector<double> H(n * n, 0.0), g(n, 0.0);
+    for (int a = 0; a < n; ++a) {
+        for (int b = 0; b < n; ++b) {
+            double s = 0;
+            for (int i = 0; i < 6; ++i) s += J[i * n + a] * W[i] * W[i] * J[i * n + b];
+            H[a * n + b] = s;
+        }
+        double d = 0;
+        for (int i = 0; i < 6; ++i) d += J[i * n + a] * J[i * n + a];
+        H[a * n + a] += c.lambda * std::max(d, c.d_floor);
+        double s = 0;
+        for (int i = 0; i < 6; ++i) s += J[i * n + a] * W[i] * W[i] * rho[i];
+        g[a] = -s;
+    }
+    return cholesky_solve(H, n, g.data(), dth);
+}
+
+/* Eqs. 14-15, readings R23: GD = -alpha_c J^T rho (Cauchy alpha),
+ * GN = -(J^T J + d_floor I)^-1 J^T rho, dtheta(tau) = tau GD + (1-tau) GN with
+ * the smallest tau in [0,1] such that |dtheta(tau)| <= R; none -> GD scaled to
+ * |.| = R.  Returns false on a zero gradient. */
+bool dogleg_step(const OracleConfig& c, const double* J, int n, const double rho[6], double* dth) {
+    std::vector<double> g0(n, 0.0);
+    double gg = 0;
+    for (int a = 0; a < n; ++a) {
+        double s = 0;
+        for (int i = 0; i < 6; ++i) s += J[i * n + a] * rho[i];
+        g0[a] = s;
+        gg += s * s;
+    }
+    if (gg <= 1e-30) return false;
+    double jg2 = 0;
+    for (int i = 0; i < 6; ++i) {
+        double s = 0;
+        for (int a = 0; a < n; ++a) s += J[i * n + a] * g0[a];
+        jg2 += s * s;
+    }
+    if (!(jg2 > 0)) return false;
+    double alpha = gg / jg2;
+    std::vector<double> gd(n), gn(n);
+    for (int a = 0; a < n; ++a) gd[a] = -alpha * g0[a];
+    std::vector<double> H(n * n, 0.0), rhs(n);
+    for (int a = 0; a < n; ++a) {
+        for (int b = 0; b < n; ++b) {
+            double s = 0;
+            for (int i = 0; i < 6; ++i) s += J[i * n + a] * J[i * n + b];
+            H[a * n + b] = s;
+        }
+        H[a * n + a] += c.d_floor;
+        rhs[a] = -g0[a];
+    }
+    if (!cholesky_solve(H, n, rhs.data(), gn.data())) return false;
+    double ngn2 = 0;
+    for (int a = 0; a < n; ++a) ngn2 += gn[a] * gn[a];
+    double R2 = c.R * c.R;
+    if (ngn2 <= R2) { for (int a = 0; a < n; ++a) dth[a] = gn[a]; return true; }
+    /* |gn + tau (gd - gn)|^2 = R^2  ->  qa tau^2 + qb tau + qc = 0 */
+    double qa = 0, qb = 0, qc = ngn2 - R2;
+    for (int a = 0; a < n; ++a) {
+        double d = gd[a] - gn[a];
+        qa += d * d;
+        qb += 2.0 * gn[a] * d;
+    }
+    double disc = qb * qb - 4.0 * qa * qc;
+    if (qa > 0 && disc >= 0) {
+        double tau = (-qb - std::sqrt(disc)) / (2.0 * qa);
+        if (tau >= 0.0 && tau <= 1.0) {
+            for (int a = 0; a < n; ++a) dth[a] = tau * gd[a] + (1.0 - tau) * gn[a];
+            return true;
+        }
+    }
+    double ngd = 0;
+    for (int a = 0; a < n; ++a) ngd += gd[a] * gd[a];
+    ngd = std::sqrt(ngd);
+    for (int a = 0; a < n; ++a) dth[a] = gd[a] * (c.R / ngd);
+    return true;
+}
+
+/* Eq. 16, reading R24: i* = argmax |g_i|, g = J^T W^2 rho; step
+ * -sign(g_i*) min(|g_i*|, R) e_i*.  Returns i* or -1 on a zero gradient. */
+int single_coord_step(const OracleConfig& c, const double* J, int n, const double W[6],
+                      const double rho[6], double* dth, double* gap) {
+    std::vector<double> g(n);
+    for (int a = 0; a < n; ++a) {
+        double s = 0;
+        for (int i = 0; i < 6; ++i) s += J[i * n + a] * W[i] * W[i] * rho[i];
+        g[a] = s;
+    }
+    int ist = 0;
+    for (int a = 1; a < n; ++a)
+        if (std::fabs(g[a]) > std::fabs(g[ist])) ist = a;
+    if (gap) {
+        double second = 0;
+        for (int a = 0; a < n; ++a)
+            if (a != ist) second = std::max(second, std::fabs(g[a]));
+        *gap = (std::fabs(g[ist]) - second) / (std::fabs(g[ist]) + 1e-300);
+    }
+    for (int a = 0; a < n; ++a) dth[a] = 0;
+    if (g[ist] == 0.0) return -1;
+    double m = std::min(std::fabs(g[ist]), c.R);
+    dth[ist] = (g[ist] > 0) ? -m : m;
+    return ist;
+}
+
+double rel_gap(double a, double b, double floor_) {
+    return std::fabs(a - b) / (std::fabs(a) + std::fabs(b) + floor_);
+}
+
+struct PolishOut { double ep, eo; int counts[4]; double margin; int iters; };
+
+/* evaluate rho at clamp(theta + alpha * dth) */
+void trial_point(const Robot& rb, const std::vector<double>& th, const double* dth, double alpha,
+                 std::vector<double>& tt) {
+    for (int j = 0; j < rb.dof; ++j) {
+        int ent = rb.dof_entry[j];
+        tt[j] = clampd(th[j] + alpha * dth[j], rb.r->lo[ent], rb.r->hi[ent]);
+    }
+}
+
+/* Eq. 13, reading R22: first alpha in {1, 1/beta, ..., 1/beta^A}
+ * with c_W(clamp(theta + alpha dth)) < c_W(theta), W frozen; returns index or -1 */
+int line_search(const Robot& rb, const OracleConfig& c, const Target& tgt,
+                const std::vector<double>& th, const double* dth, const double W[6], double c0,
+                std::vector<double>& tt, double* margin) {
+    Frames Ft;
+    double alpha = 1.0;
+    for (int a = 0; a <= c.A; ++a) {
+        trial_point(rb, th, dth, alpha, tt);
+        fk(rb, tt.data(), Ft);
+        Err et = residual(Ft, tgt);
+        double rho[6];
+        rho_of(et, rho);
+        double ct = cost_w(W, rho);
+        if (margin) *margin = std::min(*margin, rel_gap(ct, c0, 1e-30));
+        if (ct < c0) return a;
+        alpha /= c.beta;
+    }
+    return -1;
+}
+
+PolishOut pj_ik_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
+                     uint32_t bidx, std::vector<double>& th) {
+    const OracleRobot* r = rb.r;
+    int n = rb.dof;
+    PolishOut po;
+    po.margin = INF;
+    for (int i = 0; i < 4; ++i) po.counts[i] = 0;
+    Frames F, Ft;
+    std::vector<double> J(6 * n), dth(n), tt(n);
+    Err e;
+    int k;
+    for (k = 0;; ++k) {
+        fk(rb, th.data(), F);
+        e = residual(F, tgt);
+        /* Alg. 4 l.18, checked at iteration start (R26) */
+        bool cp = e.ep < c.eps_p_fine, co = e.eo < c.eps_o_fine;
+        po.margin = std::min(po.margin,
+                             margin_and(cp, rel_gap(e.ep, c.eps_p_fine, 0), co,
+                                        rel_gap(e.eo, c.eps_o_fine, 0)));
+        if (cp && co) break;
+        if (k == c.lm_iters) break;
+        jacobian(rb, F, J.data());
+        double W[6], rho[6];
+        weights(c, J.data(), n, W);
+        rho_of(e, rho);
+        double c0 = cost_w(W, rho);
+        /* LM step (Alg. 4 l.3-9) */
+        bool ok = lm_step(c, J.data(), n, W, rho, dth.data());
+        if (ok) {
+            for (int j = 0; j < n; ++j) dth[j] = clampd(dth[j], -c.R, c.R); /* l.6, R21 */
+            int a = line_search(rb, c, tgt, th, dth.data(), W, c0, tt, &po.margin);
+            if (a >= 0) { th = tt; po.counts[0]++; continue; }
+        }
+        /* dogleg (l.10-12), acceptance on the unweighted |rho| (R23) */
+        if (dogleg_step(c, J.data(), n, rho, dth.data())) {
+            trial_point(rb, th, dth.data(), 1.0, tt);
+            fk(rb, tt.data(), Ft);
+            Err et = residual(Ft, tgt);
+            double rt[6];
+            rho_of(et, rt);
+            double n0 = norm6(rho), nt = norm6(rt);
+            po.margin = std::min(po.margin, rel_gap(nt, n0, 1e-30));
+            if (nt < n0) { th = tt; po.counts[1]++; continue; }
+        }
+        /* single coordinate (l.13-16) */
+        double gap;
+        int ist = single_coord_step(c, J.data(), n, W, rho, dth.data(), &gap);
+        if (ist >= 0) {
+            po.margin = std::min(po.margin, gap);
+            int a = line_search(rb, c, tgt, th, dth.data(), W, c0, tt, &po.margin);
+            if (a >= 0) { th = tt; po.counts[2]++; continue; }
+        }
+        /* perturbation (l.17, R25) */
+        for (int j = 0; j < n; ++j) {
+            int ent = rb.dof_entry[j];
+            double g = normal_for_joint(c.rng_seed, tid, bidx, P_PJPERT, (uint32_t)k, j);
+            th[j] = clampd(th[j] + c.sigma_lm * g, r->lo[ent], r->hi[ent]);
+        }
+        po.counts[3]++;
+    }
+    po.ep = e.ep;
+    po.eo = e.eo;
+    po.iters = k;
+    return po;
+}
+
+/* c(theta) = w_p^2 |r_p|^2 + w_o^2 |omega|^2 (R14), used for ranking and best-select */
+double rank_cost(const OracleConfig& c, double ep, double eo) {
+    return c.w_p * c.w_p * ep * ep + c.w_o * c.w_o * eo * eo;
+}
+
+/* Alg. 2 l.2-8: K rounds of argmin-and-remove == the first K of a
+ * stable sort by (cost, index); then floor(B/K) copies, copy-major order
+ * b = copy * K + rank, copy 0 clean (R15), others + N(0, sigma_rep^2), clamp. */
+void rank_and_replicate(const Robot& rb, const OracleConfig& c, uint64_t tid, const double* cost,
+                        const double* theta_nm /* [n][M] */, double* seeds_bn /* [B][n] */,
+                        int32_t* kept /* [K] */) {
+    int M = c.M, K = c.K, n = rb.dof;
+    std::vector<int> idx(M);
+    for (int m = 0; m < M; ++m) idx[m] = m;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cost[a] < cost[b]; });
+    for (int i = 0; i < K; ++i) kept[i] = idx[i];
+    int copies = c.B / K;
+    for (int b = 0; b < c.B; ++b) {
+        if (b >= copies * K) { /* unused tail slots (B not a multiple of K) */
+            for (int j = 0; j < n; ++j) seeds_bn[b * n + j] = std::numeric_limits<double>::quiet_NaN();
+            continue;
+        }
+        int rank = b % K, cp = b / K;
+        int src = idx[rank];
+        for (int j = 0; j < n; ++j) {
+            int ent = rb.dof_entry[j];
+            double v = theta_nm[j * M + src];
+            if (cp > 0 || c.repl_noise_all) {
+                double g = normal_for_joint(c.rng_seed, tid, (uint32_t)b, P_REPL, 0, j);
+                v = clampd(v + c.sigma_rep * g, rb.r->lo[ent], rb.r->hi[ent]);
+            }
+            seeds_bn[b * n + j] = v;
+        }
+    }
+}
+
+} /* namespace */
+
+/* =========================== C entry points =========================== */
+extern "C" {
+
+int oracle_dof(const OracleRobot* r) { return make_robot(r).dof; }
+
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    philox4x32_10(ctr, key, out);
+}
+
+/* batched FK (+ optional frames, Jacobian): theta [N][n] -> pose [N][7]
+ * (px py pz qw qx qy qz, w >= 0), P/z [N][n][3], J [N][6][n] */
+void oracle_fk(const OracleRobot* r, const double* theta, int32_t N, double* pose, double* Pf,
+               double* zf, double* J) {
+    Robot rb = make_robot(r);
+    int n = rb.dof;
+#pragma omp parallel for schedule(static)
+    for (int s = 0; s < N; ++s) {
+        Frames F;
+        fk(rb, theta + (size_t)s * n, F);
+        double* p = pose + (size_t)s * 7;
+        p[0] = F.pee.x; p[1] = F.pee.y; p[2] = F.pee.z;
+        p[3] = F.qee.w; p[4] = F.qee.x; p[5] = F.qee.y; p[6] = F.qee.z;
+        for (int j = 0; j < n; ++j) {
+            if (Pf) { double* q = Pf + ((size_t)s * n + j) * 3; q[0] = F.P[j].x; q[1] = F.P[j].y; q[2] = F.P[j].z; }
+            if (zf) { double* q = zf + ((size_t)s * n + j) * 3; q[0] = F.z[j].x; q[1] = F.z[j].y; q[2] = F.z[j].z; }
+        }
+        if (J) jacobian(rb, F, J + (size_t)s * 6 * n);
+    }
+}
+
+void oracle_quat_error(const double qt[4], const double qe[4], double omega[3]) {
+    Qt a = {qt[0], qt[1], qt[2], qt[3]}, b = {qe[0], qe[1], qe[2], qe[3]};
+    V3 w = quat_error(a, b);
+    omega[0] = w.x; omega[1] = w.y; omega[2] = w.z;
+}
+
+void oracle_angle_axis(const double qt[4], const double qe[4], double* phi, double a[3]) {
+    Qt x = {qt[0], qt[1], qt[2], qt[3]}, y = {qe[0], qe[1], qe[2], qe[3]};
+    V3 ax;
+    angle_axis(x, y, phi, &ax);
+    a[0] = ax.x; a[1] = ax.y; a[2] = ax.z;
+}
+
+double oracle_ccd_position_step(const double Pj[3], const double rj[3], const double pee[3],
+                                const double pt[3], double tau) {
+    return ccd_position_step(v3(Pj[0], Pj[1], Pj[2]), v3(rj[0], rj[1], rj[2]),
+                             v3(pee[0], pee[1], pee[2]), v3(pt[0], pt[1], pt[2]), tau, nullptr);
+}
+
+double oracle_ccd_orientation_step(const OracleConfig* c, const double qt[4], const double qe[4],
+                                   const double rj[3], int32_t k) {
+    Qt x = {qt[0], qt[1], qt[2], qt[3]}, y = {qe[0], qe[1], qe[2], qe[3]};
+    double phi; V3 a;
+    angle_axis(x, y, &phi, &a);
+    return ccd_orientation_step(phi, a, v3(rj[0], rj[1], rj[2]), delta_k(*c, k));
+}
+
+/* LM / dogleg / single-coordinate / line-search units on explicit J, rho, W */
+int32_t oracle_lm_step(const OracleConfig* c, const double* J, int32_t n, const double W[6],
+                       const double rho[6], double* dth) {
+    return lm_step(*c, J, n, W, rho, dth) ? 1 : 0;
+}
+int32_t oracle_dogleg_step(const OracleConfig* c, const double* J, int32_t n, const double rho[6],
+                           double* dth) {
+    return dogleg_step(*c, J, n, rho, dth) ? 1 : 0;
+}
+int32_t oracle_single_coord_step(const OracleConfig* c, const double* J, int32_t n,
+                                 const double W[6], const double rho[6], double* dth) {
+    return single_coord_step(*c, J, n, W, rho, dth, nullptr);
+}
+void oracle_weights(const OracleConfig* c, const double* J, int32_t n, double W[6]) {
+    weights(*c, J, n, W);
+}
+/* line search at theta along dth toward target t7 with W frozen at theta */
+int32_t oracle_line_search(const OracleRobot* r, const OracleConfig* c, const float* t7,
+                           const double* theta, const double* dth) {
+    Robot rb = make_robot(r);
+    Target tgt = read_target(t7);
+    std::vector<double> th(theta, theta + rb.dof), tt(rb.dof), J(6 * rb.dof);
+    Frames F;
+    fk(rb, th.data(), F);
+    Err e = residual(F, tgt);
+    jacobian(rb, F, J.data());
+    double W[6], rho[6];
+    weights(*c, J.data(), rb.dof, W);
+    rho_of(e, rho);
+    return line_search(rb, *c, tgt, th, dth, W, cost_w(W, rho), tt, nullptr);
+}
+
+void oracle_uniform_seeds(const OracleRobot* r, uint64_t seed, int64_t tid, int32_t M,
+                          double* theta_nm /* [n][M] */) {
+    Robot rb = make_robot(r);
+    std::vector<double> th(rb.dof);
+    for (int m = 0; m < M; ++m) {
+        uniform_seed(rb, seed, (uint64_t)tid, (uint32_t)m, th.data());
+        for (int j = 0; j < rb.dof; ++j) theta_nm[(size_t)j * M + m] = th[j];
+    }
+}
+
+/* one standard normal of stream (tid, sid, purpose, iter) for joint d */
+double oracle_normal(uint64_t seed, int64_t tid, uint32_t sid, uint32_t purpose, uint32_t iter,
+                     int32_t d) {
+    return normal_for_joint(seed, (uint64_t)tid, sid, purpose, iter, d);
+}
+
+/* PO-CCD stage (Alg. 3) for T targets x M seeds.
+ * targets f32 [T][7]; seeds f64 [T][n][M] or NULL (Philox uniform);
+ * out: theta f64 [T][n][M], cost f64 [T][M], ep/eo f64 [T][M], iters i32 [T][M],
+ * margin f64 [T][M] (smallest absolute decision margin along the trajectory). */
+void oracle_po_ccd(const OracleRobot* r, const OracleConfig* c, const float* targets, int32_t T,
+                   int64_t tid_offset, const double* seeds, double* theta, double* cost,
+                   double* ep, double* eo, int32_t* iters, double* margin) {
+    Robot rb = make_robot(r);
+    int n = rb.dof, M = c->M;
+#pragma omp parallel for collapse(2) schedule(dynamic, 4)
+    for (int t = 0; t < T; ++t) {
+        for (int m = 0; m < M; ++m) {
+            Target tgt = read_target(targets + (size_t)t * 7);
+            uint64_t tid = (uint64_t)(tid_offset + t);
+            std::vector<double> th(n);
+            if (seeds) for (int j = 0; j < n; ++j) th[j] = seeds[((size_t)t * n + j) * M + m];
+            else uniform_seed(rb, c->rng_seed, tid, (uint32_t)m, th.data());
+            SeedOut so = po_ccd_seed(rb, *c, tgt, tid, (uint32_t)m, th);
+            for (int j = 0; j < n; ++j) theta[((size_t)t * n + j) * M + m] = th[j];
+            size_t o = (size_t)t * M + m;
+            if (cost) cost[o] = rank_cost(*c, so.ep, so.eo);
+            if (ep) ep[o] = so.ep;
+            if (eo) eo[o] = so.eo;
+            if (iters) iters[o] = so.iters;
+            if (margin) margin[o] = so.margin;
+        }
+    }
+}
+
+/* top-K + replicate (Alg. 2 l.2-8): cost f64 [T][M], theta f64 [T][n][M] ->
+ * polish seeds f64 [T][B][n], kept i32 [T][K] */
+void oracle_select_replicate(const OracleRobot* r, const OracleConfig* c, const double* cost,
+                             const double* theta, int32_t T, int64_t tid_offset, double* seeds,
+                             int32_t* kept) {
+    Robot rb = make_robot(r);
+    int n = rb.dof;
+#pragma omp parallel for schedule(static)
+    for (int t = 0; t < T; ++t)
+        rank_and_replicate(rb, *c, (uint64_t)(tid_offset + t), cost + (size_t)t * c->M,
+                           theta + (size_t)t * n * c->M, seeds + (size_t)t * c->B * n,
+                           kept + (size_t)t * c->K);
+}
+
+/* PJ-IK stage (Alg. 4): seeds f64 [T][B][n] -> theta f64 [T][B][n], ep/eo f64
+ * [T][B], counts i32 [T][B][4] (LM, dogleg, single, perturb), margin f64 [T][B]
+ * (smallest relative decision margin), iters i32 [T][B] */
+void oracle_pj_ik(const OracleRobot* r, const OracleConfig* c, const float* targets, int32_t T,
+                  int64_t tid_offset, const double* seeds, double* theta, double* ep, double* eo,
+                  int32_t* counts, double* margin, int32_t* iters) {
+    Robot rb = make_robot(r);
+    int n = rb.dof, B = c->B;
+#pragma omp parallel for collapse(2) schedule(dynamic, 2)
+    for (int t = 0; t < T; ++t) {
+        for (int b = 0; b < B; ++b) {
+            Target tgt = read_target(targets + (size_t)t * 7);
+            size_t o = (size_t)t * B + b;
+            std::vector<double> th(seeds + o * n, seeds + o * n + n);
+            PolishOut po = pj_ik_seed(rb, *c, tgt, (uint64_t)(tid_offset + t), (uint32_t)b, th);
+            for (int j = 0; j < n; ++j) theta[o * n + j] = th[j];
+            if (ep) ep[o] = po.ep;
+            if (eo) eo[o] = po.eo;
+            if (counts) for (int i = 0; i < 4; ++i) counts[o * 4 + i] = po.counts[i];
+            if (margin) margin[o] = po.margin;
+            if (iters) iters[o] = po.iters;
+        }
+    }
+}
+
+/* HJCD-IK (Alg. 2) end to end for T targets.
+ * out: q f64 [T][n], pos_err/ori_err f64 [T], status i32 [T]
+ * (0 converged at the fine tolerance, 1 success at succ_p/succ_o only,
+ *  2 not converged, 3 invalid target). */
+void oracle_solve(const OracleRobot* r, const OracleConfig* c, const float* targets, int32_t T,
+                  int64_t tid_offset, double* q_out, double* pos_err, double* ori_err,
+                  int32_t* status) {
+    Robot rb = make_robot(r);
+    int n = rb.dof, M = c->M, B = c->B, K = c->K;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int t = 0; t < T; ++t) {
+        Target tgt = read_target(targets + (size_t)t * 7);
+        uint64_t tid = (uint64_t)(tid_offset + t);
+        if (!tgt.valid) {
+            for (int j = 0; j < n; ++j) q_out[(size_t)t * n + j] = 0.0;
+            pos_err[t] = INF; ori_err[t] = INF; status[t] = 3;
+            continue;
+        }
+        /* stage 1: PO-CCD over M seeds */
+        std::vector<double> theta_nm((size_t)n * M), cost(M);
+        std::vector<double> th(n);
+        for (int m = 0; m < M; ++m) {
+            uniform_seed(rb, c->rng_seed, tid, (uint32_t)m, th.data());
+            SeedOut so = po_ccd_seed(rb, *c, tgt, tid, (uint32_t)m, th);
+            for (int j = 0; j < n; ++j) theta_nm[(size_t)j * M + m] = th[j];
+            cost[m] = rank_cost(*c, so.ep, so.eo);
+        }
+        /* top-K + replicate */
+        std::vector<double> seeds((size_t)B * n);
+        std::vector<int32_t> kept(K);
+        rank_and_replicate(rb, *c, tid, cost.data(), theta_nm.data(), seeds.data(), kept.data());
+        /* stage 2: PJ-IK over the B polish seeds, best by c(theta) (R27) */
+        int used = (B / K) * K;
+        double best = INF;
+        int bi = -1;
+        double bep = INF, beo = INF;
+        std::vector<double> bth(n, 0.0);
+        for (int b = 0; b < used; ++b) {
+            std::vector<double> s(seeds.begin() + (size_t)b * n, seeds.begin() + (size_t)b * n + n);
+            PolishOut po = pj_ik_seed(rb, *c, tgt, tid, (uint32_t)b, s);
+            double cb = rank_cost(*c, po.ep, po.eo);
+            if (cb < best) { best = cb; bi = b; bep = po.ep; beo = po.eo; bth = s; }
+        }
+        (void)bi;
+        for (int j = 0; j < n; ++j) q_out[(size_t)t * n + j] = bth[j];
+        pos_err[t] = bep;
+        ori_err[t] = beo;
+        if (bep < c->eps_p_fine && beo < c->eps_o_fine) status[t] = 0;
+        else if (bep < c->succ_p && beo < c->succ_o) status[t] = 1;
+        else status[t] = 2;
+    }
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+} /* extern "C" */
