@@ -1,0 +1,198 @@
+/*
+ * hjcd.h — C ABI of libhjcd.so, the B200 (sm_100a) hot path of HJCD-IK
+ * (arXiv 2510.07514; "P:NNN" = line of the paper's PAPER.md).
+ *
+ * Problem (Eq. 2; constraints Eq. 3): given a serial chain and
+ * target poses P_t in SE(3), find theta* with f(theta*) = P_t and
+ * theta_min <= theta* <= theta_max.  The general g(theta) >= 0 of Eq. 3 is out
+ * of scope.  Method (Alg. 2): PO-CCD over M seeds per target
+ * (Alg. 3) -> top-K + noisy replication to B seeds (Alg. 2 l.2-8,
+ * P:177-186) -> PJ-IK polish (Alg. 4) -> best of B.
+ *
+ * Conventions (every entry point):
+ *   - Plain C types only; no exceptions cross the ABI; every call returns an
+ *     hjcd_status.  Argument/shape errors are detected synchronously on the
+ *     host BEFORE any launch; kernels are then enqueued on `stream` and the
+ *     call returns without synchronising (except hjcd_solve_host).
+ *   - Ownership: the library owns only hjcd_robot handles.  Every array is
+ *     caller-owned; pointers documented "device" must be device memory of the
+ *     current CUDA device (e.g. torch tensors), "host" pointers host memory.
+ *     Scratch space is a caller-provided device workspace sized by
+ *     hjcd_workspace_size().
+ *   - Layouts are C row-major with the shapes given in brackets; all
+ *     floating point is fp32 (the kernels compute in fp32 on the FP32 ALUs).
+ *   - Pose layout: [px, py, pz, qw, qx, qy, qz] (metres, unit quaternion,
+ *     Hamilton convention, scalar first).
+ *   - Determinism: results are a pure function of (robot, config, targets,
+ *     global target ids = target_index_offset + row).  Random numbers are
+ *     Philox4x32-10 keyed by config.rng_seed with counter
+ *     (global target id, seed id, purpose << 24 | iteration, draw block), so
+ *     results do not depend on T-chunking or on the number of GPUs.
+ *   - A robot handle is immutable: it may be shared across threads, streams
+ *     and devices (it carries no device memory; the chain travels in the
+ *     kernel parameters).  Concurrent calls need distinct workspaces.
+ */
+#ifndef HJCD_H_
+#define HJCD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* hjcd_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    HJCD_OK = 0,
+    HJCD_E_INVALID_ARG = 1, /* null pointer, bad size, K > M, K > B, lo > hi, ... */
+    HJCD_E_UNSUPPORTED = 2, /* dof > HJCD_MAX_DOF, unsupported option */
+    HJCD_E_CUDA = 3,        /* a CUDA runtime error (see hjcd_last_cuda_error) */
+    HJCD_E_WORKSPACE = 4,   /* workspace too small or misaligned (< 256 B alignment) */
+    HJCD_E_NOMEM = 5        /* host allocation failed */
+} hjcd_status;
+
+#define HJCD_MAX_DOF 32
+
+/* Per-target result status written by hjcd_solve (Alg. 4 l.18). */
+enum {
+    HJCD_TARGET_CONVERGED = 0,  /* |r_p| < eps_p_fine and |omega| < eps_o_fine */
+    HJCD_TARGET_SUCCESS = 1,    /* not fine-converged but within succ_p / succ_o */
+    HJCD_TARGET_NOT_CONVERGED = 2, /* best effort returned */
+    HJCD_TARGET_INVALID = 3     /* | |q| - 1 | > 1e-3 or non-finite target; q = 0, errors = +inf */
+};
+
+typedef enum { HJCD_REVOLUTE = 0, HJCD_PRISMATIC = 1, HJCD_FIXED = 2 } hjcd_joint_type;
+
+/* One joint of a serial chain, base -> tip (D1; P:44-48 limits, P:69 axes).
+ * The joint's frame is parent * origin; it then rotates about (revolute) or
+ * translates along (prismatic) `axis`, expressed in that frame.
+ * origin_quat_wxyz must be unit (+-1e-6); axis non-zero (normalised here);
+ * lo <= hi (radians, or metres for prismatic).  Fixed joints are folded. */
+typedef struct {
+    int32_t type;
+    double origin_xyz[3];
+    double origin_quat_wxyz[4];
+    double axis[3];
+    double lo, hi;
+} hjcd_joint;
+
+typedef struct hjcd_robot hjcd_robot; /* opaque, immutable */
+
+/* Create a robot from `num_joints` joints + end-effector offset (relative to
+ * the last joint frame).  Validates (E_INVALID_ARG) and canonicalises every
+ * DoF joint to "fixed transform F_i, then rotation about / translation along
+ * local z" in fp64, stored in fp32.  dof must be 1..HJCD_MAX_DOF
+ * (E_UNSUPPORTED otherwise).  *out receives a new handle. */
+hjcd_status hjcd_robot_create(const hjcd_joint* joints, int32_t num_joints,
+                              const double ee_xyz[3], const double ee_quat_wxyz[4],
+                              hjcd_robot** out);
+
+/* DoF extension ("adding replicated revolute joints and links"; DESIGN.md
+ * R34): cyclic replication of r's DoF joints (origin, axis, limits) before the
+ * end effector until target_dof.  E_INVALID_ARG if target_dof < dof. */
+hjcd_status hjcd_robot_extend(const hjcd_robot* r, int32_t target_dof, hjcd_robot** out);
+void hjcd_robot_destroy(hjcd_robot* r);
+int32_t hjcd_robot_dof(const hjcd_robot* r);
+/* joint limits of the DoF joints as stored (fp32), host arrays [dof] */
+hjcd_status hjcd_robot_limits(const hjcd_robot* r, float* lo, float* hi);
+
+/* Algorithm parameters (Alg. 2-4 headers P:175); defaults and the
+ * reading behind each are in DESIGN.md "Readings" (R-numbers). */
+typedef struct {
+    int32_t M, K, B;               /* seeds, retained, polish batch: 1 <= K <= M, K <= B (Alg. 2) */
+    int32_t ccd_iters, lm_iters;   /* iteration budgets I_c (Alg. 3), I_l (Alg. 4) (R28) */
+    int32_t target_early_exit;     /* reserved: must be 0 (per-seed freeze is always on) */
+    float eps_p_coarse, eps_o_coarse; /* epsilon [m], nu [rad], Alg. 3 l.14 (R12) */
+    float eps_p_fine, eps_o_fine;  /* varepsilon [m], upsilon [rad], Alg. 4 l.18 (R26) */
+    float gamma;                   /* improvement threshold, Alg. 3 l.11 (R10) */
+    float delta0, delta_rho, delta_min; /* delta(k) = max(delta_min, delta0 rho^k), Eq. 11 (R5) */
+    float sigma_ccd, sigma_rep, sigma_lm; /* isotropic N(0, sigma^2) std devs (R11, R15, R25) */
+    float lambda, d_floor, R, beta; /* Eq. 12 damping, D floor, trust radius, line-search base (R20-R22) */
+    int32_t A;                     /* line-search depth: alphas 1 .. beta^-A (Eq. 13) */
+    float w_p, w_o;                /* residual weights inside W (R17) and the ranking cost (R14) */
+    float succ_p, succ_o;          /* reporting thresholds for status 1 */
+    float tau_deg;                 /* CCD degenerate-projection threshold [m] (R4) */
+    int32_t repl_noise_all;        /* 1 = noise on every replica (literal Alg. 2 l.8), 0 = copy 0 clean (R15) */
+    uint64_t rng_seed;             /* Philox key */
+    int64_t target_index_offset;   /* global id of targets[0] (RNG counter; multi-GPU shards) */
+} hjcd_config;
+
+void hjcd_config_default(hjcd_config* c);
+
+/* Bytes of device workspace hjcd_solve needs for T targets (a multiple of 256). */
+hjcd_status hjcd_workspace_size(const hjcd_robot* r, int32_t T, const hjcd_config* c, size_t* bytes);
+/* Bytes hjcd_solve_host needs: hjcd_workspace_size + device staging of I/O. */
+hjcd_status hjcd_workspace_size_host(const hjcd_robot* r, int32_t T, const hjcd_config* c,
+                                     size_t* bytes);
+
+/* HJCD-IK (Alg. 2) for T >= 1 targets.
+ *   targets  device [T][7] fp32 (pose layout above); q normalised when
+ *            | |q| - 1 | <= 1e-3, else the row gets status 3.
+ *   q_out    device [T][dof]   theta* (best polished seed, R27)
+ *   pos_err  device [T]        |P_t - P_ee(theta*)| metres
+ *   ori_err  device [T]        |omega(theta*)| radians (Eq. 5)
+ *   status   device [T]        HJCD_TARGET_*
+ *   workspace device, >= hjcd_workspace_size bytes, 256-byte aligned. */
+hjcd_status hjcd_solve(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                       float* q_out, float* pos_err, float* ori_err, int32_t* status,
+                       void* workspace, size_t workspace_bytes, hjcd_stream_t stream);
+
+/* The same with HOST buffers (same shapes): copies targets host->device,
+ * solves, copies results device->host, and synchronises `stream` before
+ * returning.  workspace: device, >= hjcd_workspace_size_host bytes. */
+hjcd_status hjcd_solve_host(const hjcd_robot* r, const hjcd_config* c, const float* targets_host,
+                            int32_t T, float* q_host, float* pos_err_host, float* ori_err_host,
+                            int32_t* status_host, void* workspace, size_t workspace_bytes,
+                            hjcd_stream_t stream);
+
+/* ---- stage entry points (tests, tracing; same conventions; device pointers) ---- */
+
+/* Batched FK (Eq. 1) + geometric Jacobian (Eq. 7) for N configurations.
+ *   q     [N][dof]; pose7 [N][7] (w >= 0); jac [N][6][dof] or NULL
+ *   (rows 0-2 linear, 3-5 angular; prismatic columns [z; 0]). */
+hjcd_status hjcd_fk(const hjcd_robot* r, const float* q, int32_t N, float* pose7, float* jac,
+                    hjcd_stream_t stream);
+
+/* PO-CCD (Alg. 3) for T targets x c->M seeds.
+ *   seeds  [T][dof][M] initial theta, or NULL = Philox uniform in limits (Alg. 3 l.2-3)
+ *   theta  [T][dof][M] out; cost [T][M] out: w_p^2 |r_p|^2 + w_o^2 |omega|^2 (R14)
+ *   pos_err, ori_err [T][M] out or NULL; iters [T][M] out or NULL (updates applied). */
+hjcd_status hjcd_poccd(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                       const float* seeds, float* theta, float* cost, float* pos_err,
+                       float* ori_err, int32_t* iters, hjcd_stream_t stream);
+
+/* Top-K by (cost, seed index) + floor(B/K) replicas (Alg. 2 l.2-8; R14, R15).
+ *   cost [T][M], theta [T][dof][M] in; polish_seeds [T][B][dof] out (slot
+ *   b = copy*K + rank; slots >= floor(B/K)*K are NaN); kept_idx [T][K] out or NULL.
+ *   Requires M <= 8192. */
+hjcd_status hjcd_select_replicate(const hjcd_robot* r, const hjcd_config* c, const float* cost,
+                                  const float* theta, int32_t T, float* polish_seeds,
+                                  int32_t* kept_idx, hjcd_stream_t stream);
+
+/* PJ-IK (Alg. 4) for T targets x c->B seeds (slots >= floor(B/K)*K skipped).
+ *   seeds [T][B][dof] in; theta [T][B][dof] out (may alias seeds);
+ *   pos_err, ori_err [T][B] out; step_counts [T][B][4] (LM, dogleg, single,
+ *   perturb) out or NULL; iters [T][B] out or NULL. */
+hjcd_status hjcd_pjik(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                      const float* seeds, float* theta, float* pos_err, float* ori_err,
+                      int32_t* step_counts, int32_t* iters, hjcd_stream_t stream);
+
+/* Best-of-B selection (Alg. 2 l.9-10, R27): argmin_b w_p^2 pe^2 + w_o^2 oe^2, ties
+ * -> lowest b; writes q_out/pos_err/ori_err/status as hjcd_solve does. */
+hjcd_status hjcd_select_best(const hjcd_robot* r, const hjcd_config* c, const float* targets,
+                             int32_t T, const float* theta, const float* pos_err_all,
+                             const float* ori_err_all, float* q_out, float* pos_err,
+                             float* ori_err, int32_t* status, hjcd_stream_t stream);
+
+const char* hjcd_status_string(hjcd_status s);
+/* text of the last CUDA error seen by this thread's calls ("" if none) */
+const char* hjcd_last_cuda_error(void);
+/* library / build identification, e.g. "hjcd 0.1 sm_100a" */
+const char* hjcd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HJCD_H_ */

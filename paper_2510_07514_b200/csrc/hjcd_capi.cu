@@ -1,0 +1,421 @@
+// hjcd_capi.cu — host side of the C ABI (include/hjcd.h): robot validation and
+// canonicalisation (fp64), config validation, workspace carving and the
+// stream-ordered launch sequence of hjcd_solve (Alg. 2).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "hjcd_internal.h"
+
+using namespace hjcd;
+
+struct hjcd_robot {
+    std::vector<hjcd_joint> joints;   // as given (for extend)
+    double ee_xyz[3];
+    double ee_quat[4];
+    int dof;
+    DevRobot dev;
+};
+
+namespace {
+
+thread_local std::string g_cuda_err;
+
+hjcd_status cuda_fail(cudaError_t e) {
+    g_cuda_err = cudaGetErrorString(e);
+    return HJCD_E_CUDA;
+}
+
+// ---------------------------------------------------------------- fp64 rigid transforms
+struct Rt {
+    double R[9];   // row-major
+    double t[3];
+};
+
+Rt rt_identity() {
+    Rt a = {{1, 0, 0, 0, 1, 0, 0, 0, 1}, {0, 0, 0}};
+    return a;
+}
+
+Rt rt_mul(const Rt& a, const Rt& b) {
+    Rt c;
+    for (int r = 0; r < 3; ++r) {
+        for (int k = 0; k < 3; ++k)
+            c.R[3 * r + k] = a.R[3 * r] * b.R[k] + a.R[3 * r + 1] * b.R[3 + k] + a.R[3 * r + 2] * b.R[6 + k];
+        c.t[r] = a.R[3 * r] * b.t[0] + a.R[3 * r + 1] * b.t[1] + a.R[3 * r + 2] * b.t[2] + a.t[r];
+    }
+    return c;
+}
+
+Rt rt_transpose_rot(const Rt& a) {   // inverse of a pure rotation
+    Rt c = rt_identity();
+    for (int r = 0; r < 3; ++r)
+        for (int k = 0; k < 3; ++k) c.R[3 * r + k] = a.R[3 * k + r];
+    return c;
+}
+
+Rt rt_from_pose(const double xyz[3], const double q[4]) {
+    double w = q[0], x = q[1], y = q[2], z = q[3];
+    double nq = std::sqrt(w * w + x * x + y * y + z * z);
+    w /= nq; x /= nq; y /= nq; z /= nq;
+    Rt a;
+    a.R[0] = 1 - 2 * (y * y + z * z); a.R[1] = 2 * (x * y - w * z); a.R[2] = 2 * (x * z + w * y);
+    a.R[3] = 2 * (x * y + w * z); a.R[4] = 1 - 2 * (x * x + z * z); a.R[5] = 2 * (y * z - w * x);
+    a.R[6] = 2 * (x * z - w * y); a.R[7] = 2 * (y * z + w * x); a.R[8] = 1 - 2 * (x * x + y * y);
+    a.t[0] = xyz[0]; a.t[1] = xyz[1]; a.t[2] = xyz[2];
+    return a;
+}
+
+// a rotation C with C e_z = a (a unit)
+Rt rot_z_to(const double a[3]) {
+    Rt C = rt_identity();
+    if (a[2] > 1.0 - 1e-15) return C;
+    if (a[2] < -1.0 + 1e-15) {   // Rx(pi)
+        C.R[4] = -1; C.R[8] = -1;
+        return C;
+    }
+    // axis k = e_z x a / |.|, angle acos(a_z)
+    double kx = -a[1], ky = a[0];
+    double s = std::sqrt(kx * kx + ky * ky);
+    kx /= s; ky /= s;
+    double c = a[2], sn = s, v = 1 - c;
+    C.R[0] = c + kx * kx * v; C.R[1] = kx * ky * v;      C.R[2] = ky * sn;
+    C.R[3] = ky * kx * v;     C.R[4] = c + ky * ky * v;  C.R[5] = -kx * sn;
+    C.R[6] = -ky * sn;        C.R[7] = kx * sn;          C.R[8] = c;
+    return C;
+}
+
+void store(const Rt& a, float R[9], float t[3]) {
+    for (int i = 0; i < 9; ++i) R[i] = (float)a.R[i];
+    for (int i = 0; i < 3; ++i) t[i] = (float)a.t[i];
+}
+
+bool finite3(const double* v, int k) {
+    for (int i = 0; i < k; ++i)
+        if (!std::isfinite(v[i])) return false;
+    return true;
+}
+
+hjcd_status build_robot(const hjcd_joint* joints, int32_t num, const double ee_xyz[3],
+                        const double ee_quat[4], hjcd_robot** out) {
+    if (!joints || num < 1 || !ee_xyz || !ee_quat || !out) return HJCD_E_INVALID_ARG;
+    int dof = 0;
+    for (int i = 0; i < num; ++i) {
+        const hjcd_joint& j = joints[i];
+        if (j.type != HJCD_REVOLUTE && j.type != HJCD_PRISMATIC && j.type != HJCD_FIXED) return HJCD_E_INVALID_ARG;
+        if (!finite3(j.origin_xyz, 3) || !finite3(j.origin_quat_wxyz, 4)) return HJCD_E_INVALID_ARG;
+        const double* q = j.origin_quat_wxyz;
+        double nq = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+        if (std::fabs(nq - 1.0) > 1e-6) return HJCD_E_INVALID_ARG;
+        if (j.type != HJCD_FIXED) {
+            if (!finite3(j.axis, 3)) return HJCD_E_INVALID_ARG;
+            double na = std::sqrt(j.axis[0] * j.axis[0] + j.axis[1] * j.axis[1] + j.axis[2] * j.axis[2]);
+            if (!(na > 1e-9)) return HJCD_E_INVALID_ARG;
+            if (!std::isfinite(j.lo) || !std::isfinite(j.hi) || j.lo > j.hi) return HJCD_E_INVALID_ARG;
+            dof++;
+        }
+    }
+    if (!finite3(ee_xyz, 3) || !finite3(ee_quat, 4)) return HJCD_E_INVALID_ARG;
+    {
+        double nq = std::sqrt(ee_quat[0] * ee_quat[0] + ee_quat[1] * ee_quat[1] + ee_quat[2] * ee_quat[2] +
+                              ee_quat[3] * ee_quat[3]);
+        if (std::fabs(nq - 1.0) > 1e-6) return HJCD_E_INVALID_ARG;
+    }
+    if (dof < 1 || dof > HJCD_MAX_DOF) return dof < 1 ? HJCD_E_INVALID_ARG : HJCD_E_UNSUPPORTED;
+
+    hjcd_robot* r = new (std::nothrow) hjcd_robot;
+    if (!r) return HJCD_E_NOMEM;
+    r->joints.assign(joints, joints + num);
+    for (int i = 0; i < 3; ++i) r->ee_xyz[i] = ee_xyz[i];
+    for (int i = 0; i < 4; ++i) r->ee_quat[i] = ee_quat[i];
+    r->dof = dof;
+    std::memset(&r->dev, 0, sizeof(DevRobot));
+    r->dev.n = dof;
+    // Canonicalise: Rot(a, th) = C Rz(th) C^T with C e_z = a; fold C^T and any
+    // fixed joints into the next joint's fixed transform F (or the ee).
+    Rt acc = rt_identity();
+    int d = 0;
+    for (int i = 0; i < num; ++i) {
+        const hjcd_joint& j = joints[i];
+        acc = rt_mul(acc, rt_from_pose(j.origin_xyz, j.origin_quat_wxyz));
+        if (j.type == HJCD_FIXED) continue;
+        double na = std::sqrt(j.axis[0] * j.axis[0] + j.axis[1] * j.axis[1] + j.axis[2] * j.axis[2]);
+        double a[3] = {j.axis[0] / na, j.axis[1] / na, j.axis[2] / na};
+        Rt C = rot_z_to(a);
+        Rt F = rt_mul(acc, C);
+        DevJoint& dj = r->dev.j[d];
+        store(F, dj.R, dj.t);
+        dj.lo = (float)j.lo;
+        dj.hi = (float)j.hi;
+        dj.type = j.type;
+        acc = rt_transpose_rot(C);
+        d++;
+    }
+    Rt E = rt_mul(acc, rt_from_pose(ee_xyz, ee_quat));
+    store(E, r->dev.eeR, r->dev.eet);
+    *out = r;
+    return HJCD_OK;
+}
+
+hjcd_status make_cfg(const hjcd_robot* r, const hjcd_config* c, DevCfg* d) {
+    if (!r || !c) return HJCD_E_INVALID_ARG;
+    if (c->M < 1 || c->K < 1 || c->B < 1 || c->K > c->M || c->K > c->B) return HJCD_E_INVALID_ARG;
+    if (c->ccd_iters < 0 || c->lm_iters < 0 || c->A < 0) return HJCD_E_INVALID_ARG;
+    if (c->target_early_exit != 0) return HJCD_E_UNSUPPORTED;
+    if (!(c->beta > 1.f) || !(c->lambda > 0.f) || !(c->d_floor > 0.f) || !(c->R > 0.f)) return HJCD_E_INVALID_ARG;
+    if (!(c->eps_p_coarse > 0.f) || !(c->eps_o_coarse > 0.f) || !(c->eps_p_fine > 0.f) ||
+        !(c->eps_o_fine > 0.f))
+        return HJCD_E_INVALID_ARG;
+    if (!(c->sigma_ccd >= 0.f) || !(c->sigma_rep >= 0.f) || !(c->sigma_lm >= 0.f)) return HJCD_E_INVALID_ARG;
+    if (!(c->delta_min >= 0.f) || !(c->delta0 >= 0.f) || !(c->delta_rho > 0.f)) return HJCD_E_INVALID_ARG;
+    if (!(c->tau_deg >= 0.f) || !(c->gamma >= 0.f) || !(c->w_p >= 0.f) || !(c->w_o >= 0.f)) return HJCD_E_INVALID_ARG;
+    d->M = c->M; d->K = c->K; d->B = c->B;
+    d->ccd_iters = c->ccd_iters; d->lm_iters = c->lm_iters; d->A = c->A;
+    d->copies = c->B / c->K;
+    d->repl_noise_all = c->repl_noise_all ? 1 : 0;
+    d->eps_p_coarse = c->eps_p_coarse; d->eps_o_coarse = c->eps_o_coarse;
+    d->eps_p_fine = c->eps_p_fine; d->eps_o_fine = c->eps_o_fine;
+    d->gamma = c->gamma; d->delta0 = c->delta0; d->delta_rho = c->delta_rho; d->delta_min = c->delta_min;
+    d->sigma_ccd = c->sigma_ccd; d->sigma_rep = c->sigma_rep; d->sigma_lm = c->sigma_lm;
+    d->lambda = c->lambda; d->d_floor = c->d_floor; d->R = c->R; d->inv_beta = 1.f / c->beta;
+    d->w_p = c->w_p; d->w_o = c->w_o; d->succ_p = c->succ_p; d->succ_o = c->succ_o;
+    d->tau_deg = c->tau_deg;
+    d->key0 = (uint32_t)c->rng_seed;
+    d->key1 = (uint32_t)(c->rng_seed >> 32);
+    d->tid_offset = c->target_index_offset;
+    return HJCD_OK;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+    size_t theta1, cost1, seeds2, ep2, eo2, total;
+};
+
+Layout layout(int dof, long long T, const hjcd_config* c) {
+    Layout L;
+    size_t off = 0;
+    L.theta1 = off; off += align256((size_t)T * dof * c->M * sizeof(float));
+    L.cost1 = off;  off += align256((size_t)T * c->M * sizeof(float));
+    L.seeds2 = off; off += align256((size_t)T * c->B * dof * sizeof(float));
+    L.ep2 = off;    off += align256((size_t)T * c->B * sizeof(float));
+    L.eo2 = off;    off += align256((size_t)T * c->B * sizeof(float));
+    L.total = off;
+    return L;
+}
+
+size_t host_staging(int dof, long long T) {
+    return align256((size_t)T * 7 * 4) + align256((size_t)T * dof * 4) + 3 * align256((size_t)T * 4);
+}
+
+}  // namespace
+
+extern "C" {
+
+hjcd_status hjcd_robot_create(const hjcd_joint* joints, int32_t num_joints, const double ee_xyz[3],
+                              const double ee_quat_wxyz[4], hjcd_robot** out) {
+    return build_robot(joints, num_joints, ee_xyz, ee_quat_wxyz, out);
+}
+
+hjcd_status hjcd_robot_extend(const hjcd_robot* r, int32_t target_dof, hjcd_robot** out) {
+    if (!r || !out) return HJCD_E_INVALID_ARG;
+    if (target_dof < r->dof) return HJCD_E_INVALID_ARG;
+    if (target_dof > HJCD_MAX_DOF) return HJCD_E_UNSUPPORTED;
+    std::vector<hjcd_joint> base, all = r->joints;
+    for (const hjcd_joint& j : r->joints)
+        if (j.type != HJCD_FIXED) base.push_back(j);
+    int d = r->dof;
+    for (size_t i = 0; d < target_dof; ++i, ++d) all.push_back(base[i % base.size()]);
+    return build_robot(all.data(), (int32_t)all.size(), r->ee_xyz, r->ee_quat, out);
+}
+
+void hjcd_robot_destroy(hjcd_robot* r) { delete r; }
+
+int32_t hjcd_robot_dof(const hjcd_robot* r) { return r ? r->dof : 0; }
+
+hjcd_status hjcd_robot_limits(const hjcd_robot* r, float* lo, float* hi) {
+    if (!r || !lo || !hi) return HJCD_E_INVALID_ARG;
+    for (int j = 0; j < r->dof; ++j) { lo[j] = r->dev.j[j].lo; hi[j] = r->dev.j[j].hi; }
+    return HJCD_OK;
+}
+
+void hjcd_config_default(hjcd_config* c) {
+    if (!c) return;
+    std::memset(c, 0, sizeof(*c));
+    c->M = 1000; c->K = 50; c->B = 100;            // R16
+    c->ccd_iters = 64; c->lm_iters = 128;          // R28
+    c->target_early_exit = 0;
+    c->eps_p_coarse = 5e-3f; c->eps_o_coarse = 5e-2f;   // R12
+    c->eps_p_fine = 1e-6f; c->eps_o_fine = 1e-5f;       // R26
+    c->gamma = 1e-6f;                                   // R10
+    c->delta0 = 1.f; c->delta_rho = 0.98f; c->delta_min = 0.1f;   // R5
+    c->sigma_ccd = 0.05f; c->sigma_rep = 0.02f; c->sigma_lm = 0.05f;   // R11, R15, R25
+    c->lambda = 1e-3f; c->d_floor = 1e-8f; c->R = 0.5f; c->beta = 2.f; c->A = 8;   // R20-R22
+    c->w_p = 1.f; c->w_o = 0.5f;                        // R17
+    c->succ_p = 1e-3f; c->succ_o = 0.017453292519943295f;
+    c->tau_deg = 1e-5f;                                 // R4
+    c->repl_noise_all = 0;                              // R15
+    c->rng_seed = 0;
+    c->target_index_offset = 0;
+}
+
+hjcd_status hjcd_workspace_size(const hjcd_robot* r, int32_t T, const hjcd_config* c, size_t* bytes) {
+    if (!r || !c || !bytes || T < 1) return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    *bytes = layout(r->dof, T, c).total;
+    return HJCD_OK;
+}
+
+hjcd_status hjcd_workspace_size_host(const hjcd_robot* r, int32_t T, const hjcd_config* c, size_t* bytes) {
+    hjcd_status st = hjcd_workspace_size(r, T, c, bytes);
+    if (st != HJCD_OK) return st;
+    *bytes += host_staging(r->dof, T);
+    return HJCD_OK;
+}
+
+hjcd_status hjcd_solve(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                       float* q_out, float* pos_err, float* ori_err, int32_t* status, void* workspace,
+                       size_t workspace_bytes, hjcd_stream_t stream) {
+    if (!r || !c || !targets || T < 1 || !q_out || !pos_err || !ori_err || !status || !workspace)
+        return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    if (c->M > 8192) return HJCD_E_UNSUPPORTED;
+    Layout L = layout(r->dof, T, c);
+    if (workspace_bytes < L.total || ((uintptr_t)workspace & 255)) return HJCD_E_WORKSPACE;
+    char* ws = (char*)workspace;
+    float* theta1 = (float*)(ws + L.theta1);
+    float* cost1 = (float*)(ws + L.cost1);
+    float* seeds2 = (float*)(ws + L.seeds2);
+    float* ep2 = (float*)(ws + L.ep2);
+    float* eo2 = (float*)(ws + L.eo2);
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    // Alg. 2 l.1: PO-CCD over M seeds per target
+    if ((e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s)) != cudaSuccess)
+        return cuda_fail(e);
+    // Alg. 2 l.2-8: top-K + replicate
+    if ((e = launch_select_replicate(r->dev, d, cost1, theta1, T, seeds2, nullptr, s)) != cudaSuccess)
+        return cuda_fail(e);
+    // Alg. 2 l.9 / Alg. 4: PJ-IK, in place on the replicated seeds
+    if ((e = launch_pjik(r->dev, d, targets, T, seeds2, seeds2, ep2, eo2, nullptr, nullptr, s)) != cudaSuccess)
+        return cuda_fail(e);
+    // Alg. 2 l.10: best of B
+    if ((e = launch_select_best(r->dev, d, targets, T, seeds2, ep2, eo2, q_out, pos_err, ori_err, status, s)) !=
+        cudaSuccess)
+        return cuda_fail(e);
+    return HJCD_OK;
+}
+
+hjcd_status hjcd_solve_host(const hjcd_robot* r, const hjcd_config* c, const float* targets_host, int32_t T,
+                            float* q_host, float* pos_err_host, float* ori_err_host, int32_t* status_host,
+                            void* workspace, size_t workspace_bytes, hjcd_stream_t stream) {
+    if (!r || !c || !targets_host || T < 1 || !q_host || !pos_err_host || !ori_err_host || !status_host ||
+        !workspace)
+        return HJCD_E_INVALID_ARG;
+    size_t need = 0;
+    hjcd_status st = hjcd_workspace_size(r, T, c, &need);
+    if (st != HJCD_OK) return st;
+    const size_t stage = host_staging(r->dof, T);
+    if (workspace_bytes < need + stage || ((uintptr_t)workspace & 255)) return HJCD_E_WORKSPACE;
+    char* io = (char*)workspace + need;
+    float* tg = (float*)io;            io += align256((size_t)T * 7 * 4);
+    float* q = (float*)io;             io += align256((size_t)T * r->dof * 4);
+    float* pe = (float*)io;            io += align256((size_t)T * 4);
+    float* oe = (float*)io;            io += align256((size_t)T * 4);
+    int32_t* stt = (int32_t*)io;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(tg, targets_host, (size_t)T * 7 * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return cuda_fail(e);
+    st = hjcd_solve(r, c, tg, T, q, pe, oe, stt, workspace, need, stream);
+    if (st != HJCD_OK) return st;
+    if ((e = cudaMemcpyAsync(q_host, q, (size_t)T * r->dof * 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(pos_err_host, pe, (size_t)T * 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(ori_err_host, oe, (size_t)T * 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(status_host, stt, (size_t)T * 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        return cuda_fail(e);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e);
+    return HJCD_OK;
+}
+
+hjcd_status hjcd_fk(const hjcd_robot* r, const float* q, int32_t N, float* pose7, float* jac,
+                    hjcd_stream_t stream) {
+    if (!r || !q || N < 1 || !pose7) return HJCD_E_INVALID_ARG;
+    cudaError_t e = launch_fk(r->dev, q, N, pose7, jac, (cudaStream_t)stream);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+}
+
+hjcd_status hjcd_poccd(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                       const float* seeds, float* theta, float* cost, float* pos_err, float* ori_err,
+                       int32_t* iters, hjcd_stream_t stream) {
+    if (!r || !c || !targets || T < 1 || !theta || !cost) return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    cudaError_t e = launch_poccd(r->dev, d, targets, T, seeds, theta, cost, pos_err, ori_err, iters,
+                                 (cudaStream_t)stream);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+}
+
+hjcd_status hjcd_select_replicate(const hjcd_robot* r, const hjcd_config* c, const float* cost,
+                                  const float* theta, int32_t T, float* polish_seeds, int32_t* kept_idx,
+                                  hjcd_stream_t stream) {
+    if (!r || !c || !cost || !theta || T < 1 || !polish_seeds) return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    if (c->M > 8192) return HJCD_E_UNSUPPORTED;
+    cudaError_t e = launch_select_replicate(r->dev, d, cost, theta, T, polish_seeds, kept_idx, (cudaStream_t)stream);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+}
+
+hjcd_status hjcd_pjik(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                      const float* seeds, float* theta, float* pos_err, float* ori_err, int32_t* step_counts,
+                      int32_t* iters, hjcd_stream_t stream) {
+    if (!r || !c || !targets || T < 1 || !seeds || !theta || !pos_err || !ori_err) return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    cudaError_t e = launch_pjik(r->dev, d, targets, T, seeds, theta, pos_err, ori_err, step_counts, iters,
+                                (cudaStream_t)stream);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+}
+
+hjcd_status hjcd_select_best(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                             const float* theta, const float* pos_err_all, const float* ori_err_all, float* q_out,
+                             float* pos_err, float* ori_err, int32_t* status, hjcd_stream_t stream) {
+    if (!r || !c || !targets || T < 1 || !theta || !pos_err_all || !ori_err_all || !q_out || !pos_err ||
+        !ori_err || !status)
+        return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    cudaError_t e = launch_select_best(r->dev, d, targets, T, theta, pos_err_all, ori_err_all, q_out, pos_err,
+                                       ori_err, status, (cudaStream_t)stream);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+}
+
+const char* hjcd_status_string(hjcd_status s) {
+    switch (s) {
+        case HJCD_OK: return "ok";
+        case HJCD_E_INVALID_ARG: return "invalid argument";
+        case HJCD_E_UNSUPPORTED: return "unsupported";
+        case HJCD_E_CUDA: return "CUDA error";
+        case HJCD_E_WORKSPACE: return "workspace too small or misaligned";
+        case HJCD_E_NOMEM: return "out of host memory";
+    }
+    return "unknown status";
+}
+
+const char* hjcd_last_cuda_error(void) { return g_cuda_err.c_str(); }
+
+const char* hjcd_version(void) { return "hjcd 0.1 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,232 @@
+// kin.cuh — device kinematics, quaternion algebra and Philox for the HJCD-IK
+// kernels (fp32, registers only).  "P:NNN" cites PAPER.md lines.
+//
+// All per-joint loops are `#pragma unroll` over the compile-time bound NMAX
+// with a uniform `j < rb.n` guard, so per-joint arrays stay in registers (no
+// dynamic indexing) and robot constants are constant-bank operands.
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "hjcd_internal.h"
+
+namespace hjcd {
+
+struct Quat {
+    float w, x, y, z;
+};
+
+__device__ __forceinline__ float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
+__device__ __forceinline__ float3 operator+(float3 a, float3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ float3 operator-(float3 a, float3 b) { return f3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ float3 operator*(float s, float3 a) { return f3(s * a.x, s * a.y, s * a.z); }
+__device__ __forceinline__ float dot3(float3 a, float3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ float3 cross3(float3 a, float3 b) {
+    return f3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ float clampf(float x, float lo, float hi) { return fminf(fmaxf(x, lo), hi); }
+
+// Hamilton product a (x) conj(b)
+__device__ __forceinline__ Quat qmul_conj(Quat a, Quat b) {
+    Quat r;
+    r.w = a.w * b.w + a.x * b.x + a.y * b.y + a.z * b.z;
+    r.x = -a.w * b.x + a.x * b.w - a.y * b.z + a.z * b.y;
+    r.y = -a.w * b.y + a.x * b.z + a.y * b.w - a.z * b.x;
+    r.z = -a.w * b.z - a.x * b.y + a.y * b.x + a.z * b.w;
+    return r;
+}
+
+// q_err = q_t (x) q_e^-1, canonicalised to w >= 0 (Eq. 5; reading R1)
+__device__ __forceinline__ Quat quat_err(Quat qt, Quat qe) {
+    Quat q = qmul_conj(qt, qe);
+    if (q.w < 0.f) { q.w = -q.w; q.x = -q.x; q.y = -q.y; q.z = -q.z; }
+    return q;
+}
+
+// |omega| = 2 atan2(|v|, w) for canonical q (Eq. 5: |omega| of
+// 2 atan2(|v|,|w|)/|v| * v).  Exact at v = 0.
+__device__ __forceinline__ float omega_norm(float sv, float w) { return 2.f * atan2f(sv, fabsf(w)); }
+
+// q_err (x) q(z, -d): the error after rotating the end effector about the
+// world axis z by d (q_e' = q(z, d) (x) q_e).  Inputs c2, s2 = cos, sin(d/2).
+__device__ __forceinline__ Quat qerr_rotate(Quat q, float3 z, float c2, float s2) {
+    Quat r;
+    float vz = q.x * z.x + q.y * z.y + q.z * z.z;
+    // v x z
+    float cx = q.y * z.z - q.z * z.y, cy = q.z * z.x - q.x * z.z, cz = q.x * z.y - q.y * z.x;
+    r.w = q.w * c2 + vz * s2;
+    r.x = c2 * q.x - s2 * q.w * z.x - s2 * cx;
+    r.y = c2 * q.y - s2 * q.w * z.y - s2 * cy;
+    r.z = c2 * q.z - s2 * q.w * z.z - s2 * cz;
+    return r;
+}
+
+// rotation matrix (row-major) -> unit quaternion, w >= 0 (Shepperd)
+__device__ __forceinline__ Quat quat_from_rot(const float R[9]) {
+    float tr = R[0] + R[4] + R[8];
+    Quat q;
+    if (tr > 0.f) {
+        float s = sqrtf(tr + 1.f) * 2.f;
+        float is = 1.f / s;
+        q.w = 0.25f * s;
+        q.x = (R[7] - R[5]) * is;
+        q.y = (R[2] - R[6]) * is;
+        q.z = (R[3] - R[1]) * is;
+    } else if (R[0] > R[4] && R[0] > R[8]) {
+        float s = sqrtf(1.f + R[0] - R[4] - R[8]) * 2.f;
+        float is = 1.f / s;
+        q.w = (R[7] - R[5]) * is;
+        q.x = 0.25f * s;
+        q.y = (R[1] + R[3]) * is;
+        q.z = (R[2] + R[6]) * is;
+    } else if (R[4] > R[8]) {
+        float s = sqrtf(1.f + R[4] - R[0] - R[8]) * 2.f;
+        float is = 1.f / s;
+        q.w = (R[2] - R[6]) * is;
+        q.x = (R[1] + R[3]) * is;
+        q.y = 0.25f * s;
+        q.z = (R[5] + R[7]) * is;
+    } else {
+        float s = sqrtf(1.f + R[8] - R[0] - R[4]) * 2.f;
+        float is = 1.f / s;
+        q.w = (R[3] - R[1]) * is;
+        q.x = (R[2] + R[6]) * is;
+        q.y = (R[5] + R[7]) * is;
+        q.z = 0.25f * s;
+    }
+    float inv = rsqrtf(q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z);
+    if (q.w < 0.f) inv = -inv;
+    q.w *= inv; q.x *= inv; q.y *= inv; q.z *= inv;
+    return q;
+}
+
+// Forward kinematics (Eq. 1) with frames (Eq. 7 inputs):
+// T = F_1 Rz(th_1) F_2 Rz(th_2) ... F_n Rz(th_n) EE  (prismatic: Tz).
+// FRAMES: P[j] = joint origin, Z[j] = joint axis (world), before joint motion
+// (identical after it: rotation about z fixes the axis and the origin).
+template <int NMAX, bool FRAMES>
+__device__ __forceinline__ void fk(const DevRobot& rb, const float (&th)[NMAX], float3 (&P)[NMAX],
+                                   float3 (&Z)[NMAX], float3& pe, Quat& qe) {
+    float R[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
+    float tx = 0.f, ty = 0.f, tz = 0.f;
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) {
+        if (j < rb.n) {
+            const DevJoint& J = rb.j[j];
+            tx += R[0] * J.t[0] + R[1] * J.t[1] + R[2] * J.t[2];
+            ty += R[3] * J.t[0] + R[4] * J.t[1] + R[5] * J.t[2];
+            tz += R[6] * J.t[0] + R[7] * J.t[1] + R[8] * J.t[2];
+            float N[9];
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc)
+                    N[3 * r + cc] = R[3 * r] * J.R[cc] + R[3 * r + 1] * J.R[3 + cc] + R[3 * r + 2] * J.R[6 + cc];
+            if (FRAMES) {
+                P[j] = f3(tx, ty, tz);
+                Z[j] = f3(N[2], N[5], N[8]);
+            }
+            if (J.type == HJCD_REVOLUTE) {
+                float s, c;
+                sincosf(th[j], &s, &c);
+#pragma unroll
+                for (int r = 0; r < 3; ++r) {
+                    float a = N[3 * r], b = N[3 * r + 1];
+                    R[3 * r] = c * a + s * b;
+                    R[3 * r + 1] = c * b - s * a;
+                    R[3 * r + 2] = N[3 * r + 2];
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 9; ++i) R[i] = N[i];
+                tx += th[j] * N[2];
+                ty += th[j] * N[5];
+                tz += th[j] * N[8];
+            }
+        }
+    }
+    tx += R[0] * rb.eet[0] + R[1] * rb.eet[1] + R[2] * rb.eet[2];
+    ty += R[3] * rb.eet[0] + R[4] * rb.eet[1] + R[5] * rb.eet[2];
+    tz += R[6] * rb.eet[0] + R[7] * rb.eet[1] + R[8] * rb.eet[2];
+    float E[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc)
+            E[3 * r + cc] = R[3 * r] * rb.eeR[cc] + R[3 * r + 1] * rb.eeR[3 + cc] + R[3 * r + 2] * rb.eeR[6 + cc];
+    pe = f3(tx, ty, tz);
+    qe = quat_from_rot(E);
+}
+
+// ---------------------------------------------------------------- targets
+struct Target {
+    float3 p;
+    Quat q;
+    bool valid;
+};
+
+// S2: normalise q when | |q| - 1 | <= 1e-3, else invalid (status 3 later)
+__device__ __forceinline__ Target load_target(const float* __restrict__ t7) {
+    Target t;
+    t.p = f3(__ldg(t7 + 0), __ldg(t7 + 1), __ldg(t7 + 2));
+    float w = __ldg(t7 + 3), x = __ldg(t7 + 4), y = __ldg(t7 + 5), z = __ldg(t7 + 6);
+    float nq = sqrtf(w * w + x * x + y * y + z * z);
+    t.valid = fabsf(nq - 1.f) <= 1e-3f && isfinite(nq) && isfinite(t.p.x) && isfinite(t.p.y) &&
+              isfinite(t.p.z);
+    if (!t.valid) { w = 1.f; x = y = z = 0.f; nq = 1.f; t.p = f3(0.f, 0.f, 0.f); }
+    float inv = 1.f / nq;
+    if (w < 0.f) inv = -inv;
+    t.q.w = w * inv; t.q.x = x * inv; t.q.y = y * inv; t.q.z = z * inv;
+    return t;
+}
+
+// ---------------------------------------------------------------- Philox4x32-10 (R30)
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    }
+    return c;
+}
+
+__device__ __forceinline__ uint4 draw(const DevCfg& c, uint32_t tid, uint32_t sid, uint32_t purpose,
+                                      uint32_t iter, uint32_t blk) {
+    return philox4x32_10(make_uint4(tid, sid, (purpose << 24) | (iter & 0xFFFFFFu), blk), c.key0, c.key1);
+}
+
+// ((x >> 9) + 0.5) * 2^-23: exact in fp32, in (0, 1)
+__device__ __forceinline__ float u01(uint32_t x) { return ((float)(x >> 9) + 0.5f) * 1.1920928955078125e-07f; }
+
+// 4 standard normals from one Philox block: Box-Muller on (u0,u1), (u2,u3)
+__device__ __forceinline__ void normals4(uint4 r, float g[4]) {
+    float u0 = u01(r.x), u1 = u01(r.y), u2 = u01(r.z), u3 = u01(r.w);
+    float ra = sqrtf(-2.f * logf(u0)), rb2 = sqrtf(-2.f * logf(u2));
+    float s, c;
+    sincospif(2.f * u1, &s, &c);
+    g[0] = ra * c; g[1] = ra * s;
+    sincospif(2.f * u3, &s, &c);
+    g[2] = rb2 * c; g[3] = rb2 * s;
+}
+
+// theta <- clamp(theta + sigma * N(0, I)), stream (tid, sid, purpose, iter)
+template <int NMAX>
+__device__ __forceinline__ void perturb(const DevRobot& rb, const DevCfg& c, float (&th)[NMAX], float sigma,
+                                        uint32_t tid, uint32_t sid, uint32_t purpose, uint32_t iter) {
+#pragma unroll
+    for (int blk = 0; blk < (NMAX + 3) / 4; ++blk) {
+        if (4 * blk < rb.n) {
+            float g[4];
+            normals4(draw(c, tid, sid, purpose, iter, blk), g);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                int j = 4 * blk + e;
+                if (j < NMAX && j < rb.n) th[j] = clampf(th[j] + sigma * g[e], rb.j[j].lo, rb.j[j].hi);
+            }
+        }
+    }
+}
+
+}  // namespace hjcd

@@ -1,0 +1,221 @@
+// poccd.cu — k_poccd: stage 1 of HJCD-IK, PO-CCD (Alg. 3).
+//
+// Mapping: one thread per (target, seed).  The paper runs one block per seed
+// with two warps per joint; on B200 the per-seed work (~1.6 kflop per
+// iteration at n = 7) is far too small to amortise block-level reductions, so
+// each seed lives in one thread's registers: FK with frames (n sincos), the 2n
+// candidate steps, and EXACT O(1) candidate scoring by rigid rotation of the
+// end effector about the joint axis (K2: FK(theta + d e_j) is the
+// current end-effector pose rotated about (P_j, z_j) by d), then the greedy
+// argmins, the gamma test on the composed two-joint move, and Philox
+// perturbation.  Seeding (Alg. 3 l.2-3) is fused in.  Per-seed freeze on the
+// coarse test (Alg. 3 l.14) is deterministic.
+#include "kin.cuh"
+
+namespace hjcd {
+
+template <int NMAX>
+__global__ void __launch_bounds__(128)
+k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
+        const float* __restrict__ targets, int T, const float* __restrict__ seeds,
+        float* __restrict__ theta_out, float* __restrict__ cost_out, float* __restrict__ ep_out,
+        float* __restrict__ eo_out, int32_t* __restrict__ iters_out) {
+    const int M = c.M;
+    const int n = rb.n;
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= (long long)T * M) return;
+    const int t = (int)(gid / M);
+    const int m = (int)(gid - (long long)t * M);
+    const Target tg = load_target(targets + 7ll * t);
+    const uint32_t tid = (uint32_t)(c.tid_offset + t);
+
+    // ---- Alg. 3 l.2-3: theta ~ U(theta_min, theta_max) (fp32 fma: R30)
+    float th[NMAX];
+    if (seeds) {
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j)
+            if (j < n) th[j] = seeds[((long long)t * n + j) * M + m];
+    } else {
+#pragma unroll
+        for (int blk = 0; blk < (NMAX + 3) / 4; ++blk) {
+            if (4 * blk < n) {
+                uint4 r = draw(c, tid, (uint32_t)m, P_INIT, 0u, (uint32_t)blk);
+                uint32_t x[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    int j = 4 * blk + e;
+                    if (j < NMAX && j < n) {
+                        float lo = rb.j[j].lo, hi = rb.j[j].hi;
+                        th[j] = __fmaf_rn(__fsub_rn(hi, lo), u01(x[e]), lo);
+                    }
+                }
+            }
+        }
+    }
+
+    float3 P[NMAX], Z[NMAX];
+    float3 pe;
+    Quat qe;
+    float ep = 0.f, eo = 0.f;
+    int k;
+    for (k = 0;; ++k) {
+        fk<NMAX, true>(rb, th, P, Z, pe, qe);
+        const float3 rp = tg.p - pe;                   // r_p (Eq. 4)
+        const Quat qr = quat_err(tg.q, qe);            // q_err (Eq. 5), w >= 0
+        const float sv = sqrtf(qr.x * qr.x + qr.y * qr.y + qr.z * qr.z);
+        ep = sqrtf(dot3(rp, rp));
+        eo = omega_norm(sv, qr.w);
+        // Alg. 3 l.14: coarse test (R12), checked at iteration start
+        if (ep < c.eps_p_coarse && eo < c.eps_o_coarse) break;
+        if (k == c.ccd_iters) break;
+
+        // Eq. 10 (R2): phi = 2 atan2(|v|, w), a = v / |v|
+        const float phi = eo;
+        const float inv_sv = sv > 0.f ? 1.f / sv : 0.f;
+        const float3 ahat = f3(qr.x * inv_sv, qr.y * inv_sv, qr.z * inv_sv);
+        const float dk = fmaxf(c.delta_min, c.delta0 * powf(c.delta_rho, (float)k));   // R5
+        const float tau2 = c.tau_deg * c.tau_deg;
+
+        // ---- Alg. 3 l.6-9: per-joint candidates, scored, greedy argmin
+        float best_p = CUDART_INF_F, best_o = CUDART_INF_F;
+        int jp = 0, jo = 0;
+        float dp_best = 0.f, do_best = 0.f;
+        float3 Pp = f3(0.f, 0.f, 0.f), Zp = f3(0.f, 0.f, 1.f), Po = Pp, Zo = Zp;
+        int typ_p = HJCD_REVOLUTE;
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) {
+            if (j < n) {
+                const DevJoint& J = rb.j[j];
+                const float3 z = Z[j];
+                float dp, sp, dor, so;
+                if (J.type == HJCD_REVOLUTE) {
+                    // Eqs. 8-9 (R3): signed angle between the projections of
+                    // P_ee - P_j and P_t - P_j on the plane normal to z_j
+                    const float3 u = pe - P[j];
+                    const float3 v = tg.p - P[j];
+                    const float3 up = u - dot3(u, z) * z;
+                    const float3 vp = v - dot3(v, z) * z;
+                    float step = 0.f;
+                    if (dot3(up, up) >= tau2 && dot3(vp, vp) >= tau2)   // R4
+                        step = atan2f(dot3(z, cross3(up, vp)), dot3(up, vp));
+                    dp = clampf(th[j] + step, J.lo, J.hi) - th[j];     // R7
+                    // score: r_p' = r_p + (1 - cos d) u_perp - sin d (z x u)
+                    float s2, c2;
+                    sincosf(0.5f * dp, &s2, &c2);
+                    const float sn = 2.f * s2 * c2, omc = 2.f * s2 * s2;
+                    const float3 zxu = cross3(z, u);
+                    const float3 r2 = rp + omc * up - sn * zxu;
+                    sp = dot3(r2, r2);
+                    // Eq. 11 (R5): delta(k) sgn(a . z_j) phi, sgn(0) = 0
+                    const float az = dot3(ahat, z);
+                    const float sg = az > 0.f ? 1.f : (az < 0.f ? -1.f : 0.f);
+                    const float so_step = phi > 0.f ? dk * sg * phi : 0.f;
+                    dor = clampf(th[j] + so_step, J.lo, J.hi) - th[j];
+                    // score: |v'|^2 of q_err (x) q(z, -d) (monotone in |omega'|)
+                    sincosf(0.5f * dor, &s2, &c2);
+                    const Quat q2 = qerr_rotate(qr, z, c2, s2);
+                    so = q2.x * q2.x + q2.y * q2.y + q2.z * q2.z;
+                } else {
+                    // prismatic (R32): exact 1-D minimiser z . (P_t - P_ee)
+                    dp = clampf(th[j] + dot3(z, rp), J.lo, J.hi) - th[j];
+                    const float3 r2 = rp - dp * z;
+                    sp = dot3(r2, r2);
+                    dor = 0.f;
+                    so = sv * sv;
+                }
+                if (sp < best_p) { best_p = sp; jp = j; dp_best = dp; Pp = P[j]; Zp = z; typ_p = J.type; }
+                if (so < best_o) { best_o = so; jo = j; do_best = dor; Po = P[j]; Zo = z; }
+            }
+        }
+
+        // ---- Alg. 3 l.10 + P:201: same joint -> the larger |step|, tie -> position (R8)
+        int ja = -1, jb = -1;      // ja upstream (smaller index), jb downstream
+        float da = 0.f, db = 0.f;
+        float3 Pa = Pp, Za = Zp, Pb = Pp, Zb = Zp;
+        int ta = typ_p, tb = typ_p;
+        if (jp == jo) {
+            if (fabsf(dp_best) >= fabsf(do_best)) { jb = jp; db = dp_best; }
+            else { jb = jo; db = do_best; Pb = Po; Zb = Zo; tb = HJCD_REVOLUTE; }
+        } else if (jp < jo) {
+            ja = jp; da = dp_best; Pa = Pp; Za = Zp; ta = typ_p;
+            jb = jo; db = do_best; Pb = Po; Zb = Zo; tb = HJCD_REVOLUTE;
+        } else {
+            ja = jo; da = do_best; Pa = Po; Za = Zo; ta = HJCD_REVOLUTE;
+            jb = jp; db = dp_best; Pb = Pp; Zb = Zp; tb = typ_p;
+        }
+        // r(theta_hat) exactly: downstream joint's rigid motion first, then the
+        // upstream one, both about the pre-update frames (K3)
+        float3 p2 = pe;
+        Quat q2 = qr;
+        {
+            if (tb == HJCD_REVOLUTE) {
+                float s2, c2;
+                sincosf(0.5f * db, &s2, &c2);
+                const float3 u = p2 - Pb;
+                const float3 up = u - dot3(u, Zb) * Zb;
+                p2 = p2 - (2.f * s2 * s2) * up + (2.f * s2 * c2) * cross3(Zb, u);
+                q2 = qerr_rotate(q2, Zb, c2, s2);
+            } else {
+                p2 = p2 + db * Zb;
+            }
+            if (ja >= 0) {
+                if (ta == HJCD_REVOLUTE) {
+                    float s2, c2;
+                    sincosf(0.5f * da, &s2, &c2);
+                    const float3 u = p2 - Pa;
+                    const float3 up = u - dot3(u, Za) * Za;
+                    p2 = p2 - (2.f * s2 * s2) * up + (2.f * s2 * c2) * cross3(Za, u);
+                    q2 = qerr_rotate(q2, Za, c2, s2);
+                } else {
+                    p2 = p2 + da * Za;
+                }
+            }
+        }
+        const float3 rh = tg.p - p2;
+        const float ep_h = sqrtf(dot3(rh, rh));
+        const float eo_h = omega_norm(sqrtf(q2.x * q2.x + q2.y * q2.y + q2.z * q2.z), q2.w);
+        // ---- Alg. 3 l.11-13 (R10): accept on an improvement > gamma in either space
+        if ((ep - ep_h) > c.gamma || (eo - eo_h) > c.gamma) {
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j) {
+                if (j < n) {
+                    if (j == jb) th[j] = th[j] + db;
+                    if (j == ja) th[j] = th[j] + da;
+                }
+            }
+        } else {
+            perturb<NMAX>(rb, c, th, c.sigma_ccd, tid, (uint32_t)m, P_PERTURB, (uint32_t)k);   // R11
+        }
+    }
+
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j)
+        if (j < n) theta_out[((long long)t * n + j) * M + m] = th[j];
+    const long long o = (long long)t * M + m;
+    cost_out[o] = c.w_p * c.w_p * ep * ep + c.w_o * c.w_o * eo * eo;   // R14
+    if (ep_out) ep_out[o] = ep;
+    if (eo_out) eo_out[o] = eo;
+    if (iters_out) iters_out[o] = k;
+}
+
+template <int NMAX>
+static cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+                                  const float* seeds, float* theta, float* cost, float* ep, float* eo,
+                                  int32_t* iters, cudaStream_t s) {
+    const long long total = (long long)T * c.M;
+    const int block = 128;
+    const long long grid = (total + block - 1) / block;
+    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+    k_poccd<NMAX><<<(unsigned)grid, block, 0, s>>>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+                         const float* seeds, float* theta, float* cost, float* ep, float* eo,
+                         int32_t* iters, cudaStream_t s) {
+    if (rb.n <= 8) return launch_poccd_t<8>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+    if (rb.n <= 16) return launch_poccd_t<16>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+    return launch_poccd_t<32>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+}
+
+}  // namespace hjcd

@@ -1,0 +1,192 @@
+// select.cu — per-target selection kernels.
+//   k_select_replicate: top-K of the M PO-CCD seeds by (cost, seed index) and
+//     floor(B/K) replicas with Philox noise (Alg. 2 l.2-8; R14, R15).
+//     One CTA per target; the M keys (order-preserving cost bits << 32 | index)
+//     are bitonic-sorted in shared memory, which yields exactly the K rounds of
+//     argmin-and-remove of Alg. 2 (ties -> lower index).
+//   k_select_best: argmin over the B polished seeds (Alg. 2 l.9-10, R27) with a
+//     warp-shuffle + shared-memory reduction of the same 64-bit keys.
+//   k_fk: batched FK + Jacobian (Eqs. 1, 7), one thread per configuration.
+#include "kin.cuh"
+
+namespace hjcd {
+
+// non-negative float -> order-preserving uint32 (NaN and negatives -> +inf)
+__device__ __forceinline__ uint32_t cost_bits(float x) {
+    if (!(x >= 0.f)) x = CUDART_INF_F;
+    return __float_as_uint(x);
+}
+
+__global__ void __launch_bounds__(512)
+k_select_replicate(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
+                   const float* __restrict__ cost, const float* __restrict__ theta, int Mpad,
+                   float* __restrict__ seeds, int32_t* __restrict__ kept) {
+    extern __shared__ unsigned long long keys[];
+    const int t = blockIdx.x;
+    const int M = c.M, K = c.K, B = c.B, n = rb.n;
+    const float* ct = cost + (long long)t * M;
+    for (int i = threadIdx.x; i < Mpad; i += blockDim.x)
+        keys[i] = (i < M) ? (((unsigned long long)cost_bits(__ldg(ct + i)) << 32) | (unsigned)i)
+                          : ~0ull;
+    __syncthreads();
+    // bitonic sort, ascending
+    for (int size = 2; size <= Mpad; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < (Mpad >> 1); i += blockDim.x) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = ((lo & size) == 0);
+                const unsigned long long a = keys[lo], b = keys[hi];
+                if ((a > b) == up) { keys[lo] = b; keys[hi] = a; }
+            }
+            __syncthreads();
+        }
+    }
+    if (kept)
+        for (int r = threadIdx.x; r < K; r += blockDim.x) kept[(long long)t * K + r] = (int32_t)(keys[r] & 0xffffffffu);
+    const uint32_t tid = (uint32_t)(c.tid_offset + t);
+    const int used = c.copies * K;
+    for (int e = threadIdx.x; e < B * n; e += blockDim.x) {
+        const int b = e / n, j = e - b * n;
+        float v;
+        if (b >= used) {
+            v = CUDART_NAN_F;
+        } else {
+            const int rank = b % K, cp = b / K;
+            const int src = (int)(keys[rank] & 0xffffffffu);
+            v = theta[((long long)t * n + j) * M + src];
+            if (cp > 0 || c.repl_noise_all) {
+                float g[4];
+                normals4(draw(c, tid, (uint32_t)b, P_REPL, 0u, (uint32_t)(j >> 2)), g);
+                v = clampf(v + c.sigma_rep * g[j & 3], rb.j[j].lo, rb.j[j].hi);
+            }
+        }
+        seeds[((long long)t * B + b) * n + j] = v;
+    }
+}
+
+__global__ void __launch_bounds__(128)
+k_select_best(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
+              const float* __restrict__ targets, const float* __restrict__ theta,
+              const float* __restrict__ ep_all, const float* __restrict__ eo_all,
+              float* __restrict__ q_out, float* __restrict__ pos_err, float* __restrict__ ori_err,
+              int32_t* __restrict__ status) {
+    __shared__ unsigned long long red[32];
+    const int t = blockIdx.x;
+    const int n = rb.n, B = c.B;
+    const int used = c.copies * c.K;
+    unsigned long long best = ~0ull;
+    for (int b = threadIdx.x; b < used; b += blockDim.x) {
+        const float pe = ep_all[(long long)t * B + b], oe = eo_all[(long long)t * B + b];
+        const float cst = c.w_p * c.w_p * pe * pe + c.w_o * c.w_o * oe * oe;   // R14
+        const unsigned long long key = ((unsigned long long)cost_bits(cst) << 32) | (unsigned)b;
+        best = key < best ? key : best;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, best, off);
+        best = o < best ? o : best;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) red[warp] = best;
+    __syncthreads();
+    if (warp == 0) {
+        best = (lane < (int)(blockDim.x >> 5)) ? red[lane] : ~0ull;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const unsigned long long o = __shfl_xor_sync(0xffffffffu, best, off);
+            best = o < best ? o : best;
+        }
+        if (lane == 0) red[0] = best;
+    }
+    __syncthreads();
+    best = red[0];
+    const int bi = (int)(best & 0xffffffffu);
+    const float* t7 = targets + 7ll * t;
+    const float w = t7[3], x = t7[4], y = t7[5], z = t7[6];
+    const float nq = sqrtf(w * w + x * x + y * y + z * z);
+    const bool valid = fabsf(nq - 1.f) <= 1e-3f && isfinite(nq) && isfinite(t7[0]) &&
+                       isfinite(t7[1]) && isfinite(t7[2]);
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+        q_out[(long long)t * n + j] = valid ? theta[((long long)t * B + bi) * n + j] : 0.f;
+    if (threadIdx.x == 0) {
+        const float pe = valid ? ep_all[(long long)t * B + bi] : CUDART_INF_F;
+        const float oe = valid ? eo_all[(long long)t * B + bi] : CUDART_INF_F;
+        pos_err[t] = pe;
+        ori_err[t] = oe;
+        int32_t s;
+        if (!valid) s = HJCD_TARGET_INVALID;
+        else if (pe < c.eps_p_fine && oe < c.eps_o_fine) s = HJCD_TARGET_CONVERGED;
+        else if (pe < c.succ_p && oe < c.succ_o) s = HJCD_TARGET_SUCCESS;
+        else s = HJCD_TARGET_NOT_CONVERGED;
+        status[t] = s;
+    }
+}
+
+template <int NMAX>
+__global__ void __launch_bounds__(128)
+k_fk(const __grid_constant__ DevRobot rb, const float* __restrict__ q, int N, float* __restrict__ pose7,
+     float* __restrict__ jac) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= N) return;
+    const int n = rb.n;
+    float th[NMAX];
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) th[j] = (j < n) ? q[(long long)s * n + j] : 0.f;
+    float3 P[NMAX], Z[NMAX], pe;
+    Quat qe;
+    fk<NMAX, true>(rb, th, P, Z, pe, qe);
+    float* o = pose7 + 7ll * s;
+    o[0] = pe.x; o[1] = pe.y; o[2] = pe.z;
+    o[3] = qe.w; o[4] = qe.x; o[5] = qe.y; o[6] = qe.z;
+    if (jac) {
+        float* J = jac + 6ll * n * s;
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) {
+            if (j < n) {
+                float3 a, b;
+                if (rb.j[j].type == HJCD_REVOLUTE) { a = cross3(Z[j], pe - P[j]); b = Z[j]; }
+                else { a = Z[j]; b = f3(0.f, 0.f, 0.f); }
+                J[0 * n + j] = a.x; J[1 * n + j] = a.y; J[2 * n + j] = a.z;
+                J[3 * n + j] = b.x; J[4 * n + j] = b.y; J[5 * n + j] = b.z;
+            }
+        }
+    }
+}
+
+cudaError_t launch_select_replicate(const DevRobot& rb, const DevCfg& c, const float* cost,
+                                    const float* theta, int T, float* seeds, int32_t* kept,
+                                    cudaStream_t s) {
+    int Mpad = 2;
+    while (Mpad < c.M) Mpad <<= 1;
+    const size_t smem = (size_t)Mpad * sizeof(unsigned long long);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_select_replicate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             8192 * (int)sizeof(unsigned long long));
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int block = Mpad >= 1024 ? 512 : (Mpad >= 256 ? 256 : 128);
+    k_select_replicate<<<T, block, smem, s>>>(rb, c, cost, theta, Mpad, seeds, kept);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_select_best(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+                               const float* theta, const float* ep_all, const float* eo_all,
+                               float* q_out, float* pos_err, float* ori_err, int32_t* status,
+                               cudaStream_t s) {
+    k_select_best<<<T, 128, 0, s>>>(rb, c, targets, theta, ep_all, eo_all, q_out, pos_err, ori_err, status);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, float* jac, cudaStream_t s) {
+    const int block = 128;
+    const int grid = (N + block - 1) / block;
+    if (rb.n <= 8) k_fk<8><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+    else if (rb.n <= 16) k_fk<16><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+    else k_fk<32><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+    return cudaGetLastError();
+}
+
+}  // namespace hjcd

@@ -1,0 +1,307 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs.  Tolerances come from north_star (BASELINE.json):
+  * per-step FK pose and Jacobian: 1e-5 absolute (fp32 vs fp64);
+  * final per-seed errors after a fixed iteration count: 1e-4 m and 1e-3 rad;
+  * success @ 1 mm / 1 deg: within 1 percentage point.
+Discrete decisions (argmins, the gamma test, line-search comparisons) are taken
+in fp32 on the GPU and fp64 in the oracle; a seed whose trajectory meets a
+near-tie may legitimately diverge.  The oracle reports each seed's smallest
+decision margin, so the tests require (a) EVERY seed whose oracle margin is
+clear of the threshold to agree, (b) every disagreeing seed to be explained by
+a near-tie, and (c) a floor on the agreeing fraction."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from params import params
+from paper_2510_07514_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL_FK = 1e-5
+TOL_P, TOL_O = 1e-4, 1e-3
+MARGIN_ABS = 1e-4     # PO-CCD decision margin (m / rad) that fp32 cannot flip
+MARGIN_REL = 1e-2     # PJ-IK relative decision margin that fp32 cannot flip
+
+
+def T(x, dev):
+    import torch
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float32, device=dev)
+
+
+def N(t):
+    return t.detach().cpu().numpy()
+
+
+def targets_for(chain, count, start=0):
+    th = inputs.halton_configs(chain, count, start=start)
+    return oracle.fk(chain, th).astype(np.float32), th
+
+
+def quat_close(qa, qb):
+    s = np.sign(np.sum(qa * qb, axis=-1, keepdims=True))
+    s[s == 0] = 1
+    return np.abs(qa - s * qb).max()
+
+
+# ---------------------------------------------------------------- FK + Jacobian
+@pytest.mark.parametrize("name", ["panda", "fetch", "panda_x14", "panda_x24", "planar2"])
+def test_fk_jacobian_parity(hjcd_lib, cuda, name):
+    ch = inputs.planar([0.6, 0.4]) if name == "planar2" else inputs.robot(name)
+    rb = hjcd_lib.Robot(ch)
+    q = inputs.uniform_configs(ch, 4096 + 37, seed=21).astype(np.float32)
+    pose, J = hjcd_lib.fk(rb, T(q, cuda), jac=True)
+    ref, Jr = oracle.fk(ch, q.astype(np.float64), jac=True)
+    pose, J = N(pose), N(J)
+    assert np.abs(pose[:, :3] - ref[:, :3]).max() < TOL_FK
+    assert quat_close(pose[:, 3:], ref[:, 3:]) < TOL_FK
+    assert np.abs(J - Jr).max() < TOL_FK
+
+
+# ---------------------------------------------------------------- PO-CCD
+def test_poccd_fused_seeding_is_bitwise(hjcd_lib, cuda):
+    ch = inputs.panda()
+    rb = hjcd_lib.Robot(ch)
+    tg, _ = targets_for(ch, 3)
+    cfg = hjcd_lib.config_from_params(params(M=1000 + 13, ccd_iters=0, rng_seed=77,
+                                             target_index_offset=5))
+    out = hjcd_lib.poccd(rb, cfg, T(tg, cuda))
+    for t in range(3):
+        ref = oracle.uniform_seeds(ch, 77, 5 + t, 1013)
+        assert np.array_equal(N(out["theta"][t]).astype(np.float64), ref)
+
+
+def poccd_compare(hjcd_lib, cuda, ch, p, tg, seeds=None):
+    rb = hjcd_lib.Robot(ch)
+    cfg = hjcd_lib.config_from_params(p)
+    out = hjcd_lib.poccd(rb, cfg, T(tg, cuda), None if seeds is None else T(seeds, cuda))
+    ref = oracle.po_ccd(ch, p, tg, seeds=None if seeds is None else seeds.astype(np.float64))
+    ep, eo = N(out["ep"]), N(out["eo"])
+    agree = (np.abs(ep - ref["ep"]) <= TOL_P) & (np.abs(eo - ref["eo"]) <= TOL_O)
+    clean = ref["margin"] >= MARGIN_ABS
+    # the reported errors are those of the returned theta (fp64 re-evaluation)
+    th = N(out["theta"]).astype(np.float64)
+    Tn, n, M = th.shape
+    flat = th.transpose(0, 2, 1).reshape(-1, n)
+    pose = oracle.fk(ch, flat).reshape(Tn, M, 7)
+    ep64 = np.linalg.norm(pose[..., :3] - tg[:, None, :3].astype(np.float64), axis=-1)
+    assert np.abs(ep64 - ep).max() < 2e-6
+    lo, hi = ch.limits()
+    assert np.all(th >= lo[None, :, None] - 1e-7) and np.all(th <= hi[None, :, None] + 1e-7)
+    return agree, clean, ref, out
+
+
+@pytest.mark.parametrize("name,iters,floor", [
+    ("panda", 1, 0.95), ("panda", 4, 0.9), ("panda", 16, 0.7), ("panda", 64, 0.2),
+    ("fetch", 4, 0.85), ("fetch", 64, 0.1), ("panda_x14", 16, 0.5)])
+def test_poccd_per_seed_parity(hjcd_lib, cuda, name, iters, floor):
+    ch = inputs.robot(name)
+    p = params(M=300, ccd_iters=iters)
+    tg, _ = targets_for(ch, 4)
+    agree, clean, ref, _ = poccd_compare(hjcd_lib, cuda, ch, p, tg)
+    bad = clean & ~agree
+    assert not bad.any(), f"{bad.sum()} clean seeds disagree (margins {ref['margin'][bad][:5]})"
+    assert agree.mean() >= floor, agree.mean()
+
+
+def test_poccd_explicit_seeds_and_ragged(hjcd_lib, cuda):
+    ch = inputs.fetch_like8()
+    M = 131   # ragged vs the 128-thread block
+    p = params(M=M, ccd_iters=8)
+    tg, _ = targets_for(ch, 3)
+    seeds = np.stack([inputs.uniform_configs(ch, M, seed=40 + t).T for t in range(3)]).astype(np.float32)
+    agree, clean, ref, _ = poccd_compare(hjcd_lib, cuda, ch, p, tg, seeds)
+    assert not (clean & ~agree).any()
+    assert agree.mean() > 0.8
+
+
+def test_poccd_seeded_on_answer(hjcd_lib, cuda):
+    # target = FK(seed 0) -> converged at iteration 0
+    ch = inputs.panda()
+    rb = hjcd_lib.Robot(ch)
+    s = oracle.uniform_seeds(ch, 0, 0, 8)
+    tg = oracle.fk(ch, s[:, 0][None]).astype(np.float32)
+    out = hjcd_lib.poccd(rb, hjcd_lib.config_from_params(params(M=8)), T(tg, cuda))
+    assert N(out["iters"])[0, 0] == 0 and N(out["ep"])[0, 0] < 1e-6
+
+
+# ---------------------------------------------------------------- top-K + replicate
+@pytest.mark.parametrize("M,K,B", [(1000, 50, 100), (64, 8, 16), (3000, 20, 70), (5, 5, 5)])
+def test_select_replicate_parity(hjcd_lib, cuda, M, K, B):
+    ch = inputs.panda()
+    rb = hjcd_lib.Robot(ch)
+    Tn = 5
+    p = params(M=M, K=K, B=B, rng_seed=3, target_index_offset=11)
+    cost = inputs.random_costs(Tn, M, seed=M)
+    cost[0, :7] = np.nan   # NaN costs rank last on both sides
+    theta = np.stack([inputs.uniform_configs(ch, M, seed=s).T for s in range(Tn)]).astype(np.float32)
+    seeds, kept = hjcd_lib.select_replicate(rb, hjcd_lib.config_from_params(p), T(cost, cuda), T(theta, cuda))
+    cost64 = cost.astype(np.float64)
+    cost64[np.isnan(cost64)] = np.inf
+    rs, rk = oracle.select_replicate(ch, p, cost64, theta.astype(np.float64), tid_offset=11)
+    assert np.array_equal(N(kept), rk)
+    s = N(seeds).astype(np.float64)
+    used = (B // K) * K
+    assert np.array_equal(s[:, :K], rs[:, :K])                     # copy 0 bitwise
+    assert np.abs(s[:, K:used] - rs[:, K:used]).max(initial=0) < 1e-6
+    assert np.isnan(s[:, used:]).all() and np.isnan(rs[:, used:]).all()
+
+
+# ---------------------------------------------------------------- PJ-IK
+def pjik_compare(hjcd_lib, cuda, ch, p, tg, seeds):
+    rb = hjcd_lib.Robot(ch)
+    cfg = hjcd_lib.config_from_params(p)
+    out = hjcd_lib.pjik(rb, cfg, T(tg, cuda), T(seeds, cuda))
+    ref = oracle.pj_ik(ch, p, tg, seeds.astype(np.float64))
+    used = (p["B"] // p["K"]) * p["K"]
+    ep, eo = N(out["ep"])[:, :used], N(out["eo"])[:, :used]
+    agree = (np.abs(ep - ref["ep"][:, :used]) <= TOL_P) & (np.abs(eo - ref["eo"][:, :used]) <= TOL_O)
+    clean = ref["margin"][:, :used] >= MARGIN_REL
+    lo, hi = ch.limits()
+    th = N(out["theta"])[:, :used]
+    assert np.all(th >= lo - 1e-7) and np.all(th <= hi + 1e-7)
+    return agree, clean, ref, out
+
+
+@pytest.mark.parametrize("name,sigma,iters,floor", [
+    ("panda", 0.02, 32, 0.9), ("panda", 0.3, 32, 0.6), ("fetch", 0.1, 32, 0.6),
+    ("panda_x14", 0.05, 16, 0.6), ("panda", 0.3, 128, 0.5)])
+def test_pjik_per_seed_parity(hjcd_lib, cuda, name, sigma, iters, floor):
+    ch = inputs.robot(name)
+    Tn, B = 6, 40
+    p = params(B=B, K=10, lm_iters=iters)
+    tg, th0 = targets_for(ch, Tn)
+    seeds = inputs.near_configs(ch, np.repeat(th0[:, None, :], B, 1), sigma, seed=8).astype(np.float32)
+    agree, clean, ref, out = pjik_compare(hjcd_lib, cuda, ch, p, tg, seeds)
+    bad = clean & ~agree
+    assert not bad.any(), f"{bad.sum()} clean seeds disagree"
+    assert agree.mean() >= floor, agree.mean()
+
+
+def test_pjik_zero_error_fixed_point(hjcd_lib, cuda):
+    ch = inputs.panda()
+    rb = hjcd_lib.Robot(ch)
+    th0 = inputs.halton_configs(ch, 8).astype(np.float32)
+    tg = oracle.fk(ch, th0.astype(np.float64)).astype(np.float32)
+    p = params(B=4, K=2)
+    seeds = np.repeat(th0[:, None, :], 4, 1)
+    out = hjcd_lib.pjik(rb, hjcd_lib.config_from_params(p), T(tg, cuda), T(seeds, cuda))
+    assert (N(out["iters"]) == 0).all() and (N(out["counts"]) == 0).all()
+    assert np.array_equal(N(out["theta"]), seeds)
+
+
+# ---------------------------------------------------------------- end to end
+def success(pe, oe):
+    return (pe < 1e-3) & (oe < math.pi / 180)
+
+
+def fp64_errors(ch, q, tg):
+    pose = oracle.fk(ch, q.astype(np.float64))
+    pe = np.linalg.norm(pose[:, :3] - tg[:, :3].astype(np.float64), axis=1)
+    qt = tg[:, 3:].astype(np.float64)
+    qt /= np.linalg.norm(qt, axis=1, keepdims=True)
+    oe = np.array([np.linalg.norm(oracle.quat_error(a, b)) for a, b in zip(qt, pose[:, 3:])])
+    return pe, oe
+
+
+def test_c1_end_to_end_vs_oracle(hjcd_lib, cuda):
+    # BASELINE configs[0]: Panda, M=64, K=8, B=16, fixed iterations 64/32
+    ch = inputs.panda()
+    rb = hjcd_lib.Robot(ch)
+    tg, _ = targets_for(ch, 24)
+    for seed in (0, 1, 2):
+        p = params(M=64, K=8, B=16, ccd_iters=64, lm_iters=32, rng_seed=seed)
+        q, pe, oe, st = hjcd_lib.solve(rb, T(tg, cuda), hjcd_lib.config_from_params(p))
+        rq, rpe, roe, rst = oracle.solve(ch, p, tg)
+        g = success(*fp64_errors(ch, N(q), tg))
+        r = success(rpe, roe)
+        assert abs(g.mean() - r.mean()) <= 2.0 / 24 + 1e-9, (seed, g.mean(), r.mean())
+        assert np.all((N(st) <= 1) == g)
+
+
+def test_success_rate_parity(hjcd_lib, cuda):
+    # north_star: success @ 1 mm / 1 deg within 1 pp of the oracle
+    ch = inputs.panda()
+    rb = hjcd_lib.Robot(ch)
+    Tn = 100
+    tg, _ = targets_for(ch, Tn)
+    p = params(M=256, K=16, B=32)
+    q, pe, oe, st = hjcd_lib.solve(rb, T(tg, cuda), hjcd_lib.config_from_params(p))
+    rq, rpe, roe, rst = oracle.solve(ch, p, tg)
+    g = success(*fp64_errors(ch, N(q), tg)).mean()
+    r = success(rpe, roe).mean()
+    assert abs(g - r) <= 0.01 + 1e-9, (g, r)
+    assert g >= 0.99
+
+
+def test_full_size_c2(hjcd_lib, cuda):
+    """BASELINE configs[1] in bench.py's launch configuration: Panda, 1000 targets
+    x 1000 seeds, defaults.  Sampled targets vs the oracle one by one; properties
+    over all 1000."""
+    import torch
+    ch = inputs.panda()
+    rb = hjcd_lib.Robot(ch)
+    Tn = 1000
+    tg, _ = targets_for(ch, Tn)
+    p = params()
+    cfg = hjcd_lib.config_from_params(p)
+    tgd = T(tg, cuda)
+    q, pe, oe, st = hjcd_lib.solve(rb, tgd, cfg)
+    q, pe, oe, st = N(q), N(pe), N(oe), N(st)
+    pe64, oe64 = fp64_errors(ch, q, tg)
+    assert np.abs(pe64 - pe).max() < 2e-6 and np.abs(oe64 - oe).max() < 2e-5
+    assert success(pe64, oe64).mean() >= 0.99
+    lo, hi = ch.limits()
+    assert np.all(q >= lo - 1e-7) and np.all(q <= hi + 1e-7)
+    # sampled rows vs the oracle, each with its own global target id
+    for i in (0, 499, 999):
+        rq, rpe, roe, rst = oracle.solve(ch, p, tg[i:i + 1], tid_offset=i)
+        assert success(rpe, roe)[0] == success(pe64[i:i + 1], oe64[i:i + 1])[0]
+    # determinism and T-chunking invariance (RNG keyed by global target id)
+    q2, _, _, _ = hjcd_lib.solve(rb, tgd, cfg)
+    assert np.array_equal(N(q2), q)
+    c2 = hjcd_lib.config_from_params(dict(p, target_index_offset=500))
+    qa, _, _, _ = hjcd_lib.solve(rb, tgd[:500].contiguous(), cfg)
+    qb, _, _, _ = hjcd_lib.solve(rb, tgd[500:].contiguous(), c2)
+    assert np.array_equal(np.concatenate([N(qa), N(qb)]), q)
+    # host-buffer entry point gives the same bytes
+    qh, peh, oeh, sth = hjcd_lib.solve_host(rb, tg, cfg)
+    assert np.array_equal(qh.numpy(), q) and np.array_equal(sth.numpy(), st)
+    torch.cuda.synchronize()
+
+
+def test_edge_cases(hjcd_lib, cuda):
+    ch = inputs.panda()
+    rb = hjcd_lib.Robot(ch)
+    p = params(M=64, K=8, B=20, lm_iters=32)   # B not a multiple of K
+    cfg = hjcd_lib.config_from_params(p)
+    tg, _ = targets_for(ch, 3)
+    far = inputs.unreachable_targets(2, 2 * inputs.max_reach(ch), seed=1)
+    bad = tg[:1].copy(); bad[0, 3:] = [0.5, 0.5, 0.5, 0.0]   # |q| = 0.866
+    nan = tg[:1].copy(); nan[0, 0] = np.nan
+    allt = np.concatenate([tg, far, bad, nan]).astype(np.float32)
+    q, pe, oe, st = hjcd_lib.solve(rb, T(allt, cuda), cfg)
+    st, pe, q = N(st), N(pe), N(q)
+    assert np.all(st[:3] <= 1)
+    assert np.all(st[3:5] == 2) and np.all(np.isfinite(pe[3:5]))
+    assert st[5] == 3 and st[6] == 3 and np.all(q[5:] == 0) and np.isinf(pe[5])
+    # T = 1 and a 2-DoF planar arm
+    pl = inputs.planar([0.6, 0.4])
+    tg2 = oracle.fk(pl, np.array([[0.7, -1.1]])).astype(np.float32)
+    q, pe, oe, st = hjcd_lib.solve(hjcd_lib.Robot(pl), T(tg2, cuda), hjcd_lib.config_from_params(params(M=32, K=4, B=8)))
+    assert N(st)[0] == 0 and np.abs(N(q)[0] - [0.7, -1.1]).max() < 1e-3
+
+
+@pytest.mark.parametrize("name", ["fetch", "panda_x14", "panda_x24"])
+def test_solve_other_chains(hjcd_lib, cuda, name):
+    ch = inputs.robot(name)
+    rb = hjcd_lib.Robot(ch)
+    tg, _ = targets_for(ch, 32)
+    p = params(M=512, K=32, B=64)
+    q, pe, oe, st = hjcd_lib.solve(rb, T(tg, cuda), hjcd_lib.config_from_params(p))
+    pe64, oe64 = fp64_errors(ch, N(q), tg)
+    assert success(pe64, oe64).mean() >= 0.95
+    rq, rpe, roe, rst = oracle.solve(ch, p, tg[:8])
+    assert abs(success(pe64[:8], oe64[:8]).mean() - success(rpe, roe).mean()) <= 1 / 8 + 1e-9
