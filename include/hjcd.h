@@ -103,7 +103,10 @@ hjcd_status hjcd_robot_limits(const hjcd_robot* r, float* lo, float* hi);
 typedef struct {
     int32_t M, K, B;               /* seeds, retained, polish batch: 1 <= K <= M, K <= B (Alg. 2) */
     int32_t ccd_iters, lm_iters;   /* iteration budgets I_c (Alg. 3), I_l (Alg. 4) (R28) */
-    int32_t target_early_exit;     /* reserved: must be 0 (per-seed freeze is always on) */
+    int32_t target_early_exit;     /* PJ-IK stop rule (Alg. 4 l.18; R26b): 1 = a target stops at the
+                                      first iteration in which ANY of its polish seeds passes the fine
+                                      test (deterministic, needs floor(B/K)*K <= 256); 0 = every seed
+                                      runs until it converges or lm_iters (per-seed freeze) */
     float eps_p_coarse, eps_o_coarse; /* epsilon [m], nu [rad], Alg. 3 l.14 (R12) */
     float eps_p_fine, eps_o_fine;  /* varepsilon [m], upsilon [rad], Alg. 4 l.18 (R26) */
     float gamma;                   /* improvement threshold, Alg. 3 l.11 (R10) */

@@ -79,6 +79,7 @@ typedef struct {
     double tau_deg;
     uint64_t rng_seed;
     int32_t repl_noise_all;
+    int32_t target_early_exit;
 } OracleConfig;
 
 } /* extern "C" */
@@ -503,6 +504,11 @@ SeedOut po_ccd_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, u
             thh[jp] = th[jp] + dp[jp];
             thh[jo] = th[jo] + dor[jo];
         }
+        /* clamp after every applied update (R7): removes rounding overshoot */
+        for (int j = 0; j < n; ++j) {
+            int ent = rb.dof_entry[j];
+            thh[j] = clampd(thh[j], r->lo[ent], r->hi[ent]);
+        }
         fk(rb, thh.data(), Fc);
         Err eh = residual(Fc, tgt);
         /* Alg. 3 l.11 read as an improvement test on either space (R10) */
@@ -740,70 +746,113 @@ int line_search(const Robot& rb, const OracleConfig& c, const Target& tgt,
     return -1;
 }
 
-PolishOut pj_ik_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
-                     uint32_t bidx, std::vector<double>& th) {
+/* Alg. 4 l.18 fine test at iteration start (R26); stores the residual */
+bool pj_ik_check(const Robot& rb, const OracleConfig& c, const Target& tgt,
+                 const std::vector<double>& th, Frames& F, Err& e, PolishOut& po) {
+    fk(rb, th.data(), F);
+    e = residual(F, tgt);
+    bool cp = e.ep < c.eps_p_fine, co = e.eo < c.eps_o_fine;
+    po.margin = std::min(po.margin, margin_and(cp, rel_gap(e.ep, c.eps_p_fine, 0), co,
+                                               rel_gap(e.eo, c.eps_o_fine, 0)));
+    po.ep = e.ep;
+    po.eo = e.eo;
+    return cp && co;
+}
+
+/* one iteration of Alg. 4 (l.3-17) for one seed, frames F and residual e at th */
+void pj_ik_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
+                uint32_t bidx, int k, const Frames& F, const Err& e, std::vector<double>& th,
+                PolishOut& po) {
     const OracleRobot* r = rb.r;
     int n = rb.dof;
+    Frames Ft;
+    std::vector<double> J(6 * n), dth(n), tt(n);
+    jacobian(rb, F, J.data());
+    double W[6], rho[6];
+    weights(c, J.data(), n, W);
+    rho_of(e, rho);
+    double c0 = cost_w(W, rho);
+    /* LM step (Alg. 4 l.3-9) */
+    bool ok = lm_step(c, J.data(), n, W, rho, dth.data());
+    if (ok) {
+        for (int j = 0; j < n; ++j) dth[j] = clampd(dth[j], -c.R, c.R); /* l.6, R21 */
+        int a = line_search(rb, c, tgt, th, dth.data(), W, c0, tt, &po.margin);
+        if (a >= 0) { th = tt; po.counts[0]++; return; }
+    }
+    /* dogleg (l.10-12), acceptance on the unweighted |rho| (R23) */
+    if (dogleg_step(c, J.data(), n, rho, dth.data())) {
+        trial_point(rb, th, dth.data(), 1.0, tt);
+        fk(rb, tt.data(), Ft);
+        Err et = residual(Ft, tgt);
+        double rt[6];
+        rho_of(et, rt);
+        double n0 = norm6(rho), nt = norm6(rt);
+        po.margin = std::min(po.margin, rel_gap(nt, n0, 1e-30));
+        if (nt < n0) { th = tt; po.counts[1]++; return; }
+    }
+    /* single coordinate (l.13-16) */
+    double gap;
+    int ist = single_coord_step(c, J.data(), n, W, rho, dth.data(), &gap);
+    if (ist >= 0) {
+        po.margin = std::min(po.margin, gap);
+        int a = line_search(rb, c, tgt, th, dth.data(), W, c0, tt, &po.margin);
+        if (a >= 0) { th = tt; po.counts[2]++; return; }
+    }
+    /* perturbation (l.17, R25) */
+    for (int j = 0; j < n; ++j) {
+        int ent = rb.dof_entry[j];
+        double g = normal_for_joint(c.rng_seed, tid, bidx, P_PJPERT, (uint32_t)k, j);
+        th[j] = clampd(th[j] + c.sigma_lm * g, r->lo[ent], r->hi[ent]);
+    }
+    po.counts[3]++;
+}
+
+PolishOut polish_init() {
     PolishOut po;
     po.margin = INF;
+    po.ep = po.eo = INF;
+    po.iters = 0;
     for (int i = 0; i < 4; ++i) po.counts[i] = 0;
-    Frames F, Ft;
-    std::vector<double> J(6 * n), dth(n), tt(n);
+    return po;
+}
+
+/* Alg. 4 for ONE seed with a per-seed break (target_early_exit = 0) */
+PolishOut pj_ik_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
+                     uint32_t bidx, std::vector<double>& th) {
+    PolishOut po = polish_init();
+    Frames F;
     Err e;
     int k;
     for (k = 0;; ++k) {
-        fk(rb, th.data(), F);
-        e = residual(F, tgt);
-        /* Alg. 4 l.18, checked at iteration start (R26) */
-        bool cp = e.ep < c.eps_p_fine, co = e.eo < c.eps_o_fine;
-        po.margin = std::min(po.margin,
-                             margin_and(cp, rel_gap(e.ep, c.eps_p_fine, 0), co,
-                                        rel_gap(e.eo, c.eps_o_fine, 0)));
-        if (cp && co) break;
+        if (pj_ik_check(rb, c, tgt, th, F, e, po)) break;
         if (k == c.lm_iters) break;
-        jacobian(rb, F, J.data());
-        double W[6], rho[6];
-        weights(c, J.data(), n, W);
-        rho_of(e, rho);
-        double c0 = cost_w(W, rho);
-        /* LM step (Alg. 4 l.3-9) */
-        bool ok = lm_step(c, J.data(), n, W, rho, dth.data());
-        if (ok) {
-            for (int j = 0; j < n; ++j) dth[j] = clampd(dth[j], -c.R, c.R); /* l.6, R21 */
-            int a = line_search(rb, c, tgt, th, dth.data(), W, c0, tt, &po.margin);
-            if (a >= 0) { th = tt; po.counts[0]++; continue; }
-        }
-        /* dogleg (l.10-12), acceptance on the unweighted |rho| (R23) */
-        if (dogleg_step(c, J.data(), n, rho, dth.data())) {
-            trial_point(rb, th, dth.data(), 1.0, tt);
-            fk(rb, tt.data(), Ft);
-            Err et = residual(Ft, tgt);
-            double rt[6];
-            rho_of(et, rt);
-            double n0 = norm6(rho), nt = norm6(rt);
-            po.margin = std::min(po.margin, rel_gap(nt, n0, 1e-30));
-            if (nt < n0) { th = tt; po.counts[1]++; continue; }
-        }
-        /* single coordinate (l.13-16) */
-        double gap;
-        int ist = single_coord_step(c, J.data(), n, W, rho, dth.data(), &gap);
-        if (ist >= 0) {
-            po.margin = std::min(po.margin, gap);
-            int a = line_search(rb, c, tgt, th, dth.data(), W, c0, tt, &po.margin);
-            if (a >= 0) { th = tt; po.counts[2]++; continue; }
-        }
-        /* perturbation (l.17, R25) */
-        for (int j = 0; j < n; ++j) {
-            int ent = rb.dof_entry[j];
-            double g = normal_for_joint(c.rng_seed, tid, bidx, P_PJPERT, (uint32_t)k, j);
-            th[j] = clampd(th[j] + c.sigma_lm * g, r->lo[ent], r->hi[ent]);
-        }
-        po.counts[3]++;
+        pj_ik_step(rb, c, tgt, tid, bidx, k, F, e, th, po);
     }
-    po.ep = e.ep;
-    po.eo = e.eo;
     po.iters = k;
     return po;
+}
+
+/* Alg. 4 for the `used` seeds of ONE target in the paper's loop order: the
+ * iteration loop outside, the seeds inside.  target_early_exit = 1:
+ * the target stops at the first iteration at which any seed passes the fine
+ * test (Alg. 4 l.18 "break"), every seed keeping its state after
+ * the same number of iterations (R26b).  th_bn: [used][n] in/out. */
+void pj_ik_target(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid, int used,
+                  std::vector<std::vector<double>>& th_bn, std::vector<PolishOut>& po) {
+    po.assign(used, polish_init());
+    std::vector<Frames> F(used);
+    std::vector<Err> e(used);
+    for (int k = 0;; ++k) {
+        bool any = false;
+        for (int b = 0; b < used; ++b) {
+            bool cv = pj_ik_check(rb, c, tgt, th_bn[b], F[b], e[b], po[b]);
+            any = any || cv;
+        }
+        for (int b = 0; b < used; ++b) po[b].iters = k;
+        if (any || k == c.lm_iters) break;
+        for (int b = 0; b < used; ++b)
+            pj_ik_step(rb, c, tgt, tid, (uint32_t)b, k, F[b], e[b], th_bn[b], po[b]);
+    }
 }
 
 /* c(theta) = w_p^2 |r_p|^2 + w_o^2 |omega|^2 (R14), used for ranking and best-select */
@@ -1000,19 +1049,38 @@ void oracle_pj_ik(const OracleRobot* r, const OracleConfig* c, const float* targ
                   int32_t* counts, double* margin, int32_t* iters) {
     Robot rb = make_robot(r);
     int n = rb.dof, B = c->B;
+    int used = (c->B / c->K) * c->K;
+    auto emit = [&](size_t o, const std::vector<double>& th, const PolishOut& po) {
+        for (int j = 0; j < n; ++j) theta[o * n + j] = th[j];
+        if (ep) ep[o] = po.ep;
+        if (eo) eo[o] = po.eo;
+        if (counts) for (int i = 0; i < 4; ++i) counts[o * 4 + i] = po.counts[i];
+        if (margin) margin[o] = po.margin;
+        if (iters) iters[o] = po.iters;
+    };
+    if (c->target_early_exit) {
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int t = 0; t < T; ++t) {
+            Target tgt = read_target(targets + (size_t)t * 7);
+            std::vector<std::vector<double>> th(used);
+            for (int b = 0; b < used; ++b) {
+                size_t o = (size_t)t * B + b;
+                th[b].assign(seeds + o * n, seeds + o * n + n);
+            }
+            std::vector<PolishOut> po;
+            pj_ik_target(rb, *c, tgt, (uint64_t)(tid_offset + t), used, th, po);
+            for (int b = 0; b < used; ++b) emit((size_t)t * B + b, th[b], po[b]);
+        }
+        return;
+    }
 #pragma omp parallel for collapse(2) schedule(dynamic, 2)
     for (int t = 0; t < T; ++t) {
-        for (int b = 0; b < B; ++b) {
+        for (int b = 0; b < used; ++b) {
             Target tgt = read_target(targets + (size_t)t * 7);
             size_t o = (size_t)t * B + b;
             std::vector<double> th(seeds + o * n, seeds + o * n + n);
             PolishOut po = pj_ik_seed(rb, *c, tgt, (uint64_t)(tid_offset + t), (uint32_t)b, th);
-            for (int j = 0; j < n; ++j) theta[o * n + j] = th[j];
-            if (ep) ep[o] = po.ep;
-            if (eo) eo[o] = po.eo;
-            if (counts) for (int i = 0; i < 4; ++i) counts[o * 4 + i] = po.counts[i];
-            if (margin) margin[o] = po.margin;
-            if (iters) iters[o] = po.iters;
+            emit(o, th, po);
         }
     }
 }
@@ -1050,17 +1118,22 @@ void oracle_solve(const OracleRobot* r, const OracleConfig* c, const float* targ
         rank_and_replicate(rb, *c, tid, cost.data(), theta_nm.data(), seeds.data(), kept.data());
         /* stage 2: PJ-IK over the B polish seeds, best by c(theta) (R27) */
         int used = (B / K) * K;
+        std::vector<std::vector<double>> th2(used);
+        std::vector<PolishOut> po(used);
+        for (int b = 0; b < used; ++b)
+            th2[b].assign(seeds.begin() + (size_t)b * n, seeds.begin() + (size_t)b * n + n);
+        if (c->target_early_exit) {
+            pj_ik_target(rb, *c, tgt, tid, used, th2, po);
+        } else {
+            for (int b = 0; b < used; ++b) po[b] = pj_ik_seed(rb, *c, tgt, tid, (uint32_t)b, th2[b]);
+        }
         double best = INF;
-        int bi = -1;
         double bep = INF, beo = INF;
         std::vector<double> bth(n, 0.0);
         for (int b = 0; b < used; ++b) {
-            std::vector<double> s(seeds.begin() + (size_t)b * n, seeds.begin() + (size_t)b * n + n);
-            PolishOut po = pj_ik_seed(rb, *c, tgt, tid, (uint32_t)b, s);
-            double cb = rank_cost(*c, po.ep, po.eo);
-            if (cb < best) { best = cb; bi = b; bep = po.ep; beo = po.eo; bth = s; }
+            double cb = rank_cost(*c, po[b].ep, po[b].eo);
+            if (cb < best) { best = cb; bep = po[b].ep; beo = po[b].eo; bth = th2[b]; }
         }
-        (void)bi;
         for (int j = 0; j < n; ++j) q_out[(size_t)t * n + j] = bth[j];
         pos_err[t] = bep;
         ori_err[t] = beo;

@@ -164,7 +164,8 @@ hjcd_status make_cfg(const hjcd_robot* r, const hjcd_config* c, DevCfg* d) {
     if (!r || !c) return HJCD_E_INVALID_ARG;
     if (c->M < 1 || c->K < 1 || c->B < 1 || c->K > c->M || c->K > c->B) return HJCD_E_INVALID_ARG;
     if (c->ccd_iters < 0 || c->lm_iters < 0 || c->A < 0) return HJCD_E_INVALID_ARG;
-    if (c->target_early_exit != 0) return HJCD_E_UNSUPPORTED;
+    if (c->target_early_exit != 0 && c->target_early_exit != 1) return HJCD_E_INVALID_ARG;
+    if (c->target_early_exit && (c->B / c->K) * c->K > 256) return HJCD_E_UNSUPPORTED;
     if (!(c->beta > 1.f) || !(c->lambda > 0.f) || !(c->d_floor > 0.f) || !(c->R > 0.f)) return HJCD_E_INVALID_ARG;
     if (!(c->eps_p_coarse > 0.f) || !(c->eps_o_coarse > 0.f) || !(c->eps_p_fine > 0.f) ||
         !(c->eps_o_fine > 0.f))
@@ -176,6 +177,7 @@ hjcd_status make_cfg(const hjcd_robot* r, const hjcd_config* c, DevCfg* d) {
     d->ccd_iters = c->ccd_iters; d->lm_iters = c->lm_iters; d->A = c->A;
     d->copies = c->B / c->K;
     d->repl_noise_all = c->repl_noise_all ? 1 : 0;
+    d->target_early_exit = c->target_early_exit;
     d->eps_p_coarse = c->eps_p_coarse; d->eps_o_coarse = c->eps_o_coarse;
     d->eps_p_fine = c->eps_p_fine; d->eps_o_fine = c->eps_o_fine;
     d->gamma = c->gamma; d->delta0 = c->delta0; d->delta_rho = c->delta_rho; d->delta_min = c->delta_min;
@@ -247,7 +249,7 @@ void hjcd_config_default(hjcd_config* c) {
     std::memset(c, 0, sizeof(*c));
     c->M = 1000; c->K = 50; c->B = 100;            // R16
     c->ccd_iters = 64; c->lm_iters = 128;          // R28
-    c->target_early_exit = 0;
+    c->target_early_exit = 1;                           // R26b
     c->eps_p_coarse = 5e-3f; c->eps_o_coarse = 5e-2f;   // R12
     c->eps_p_fine = 1e-6f; c->eps_o_fine = 1e-5f;       // R26
     c->gamma = 1e-6f;                                   // R10

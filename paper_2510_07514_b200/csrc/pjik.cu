@@ -86,25 +86,39 @@ __device__ __forceinline__ Resid eval_at(const DevRobot& rb, const Target& tg, c
     return residual(tg, pe, qe);
 }
 
-template <int NMAX>
-__global__ void __launch_bounds__(128)
+// TEXIT = false: one thread per polish seed anywhere in the grid, per-seed break.
+// TEXIT = true : one CTA per target, thread b = polish slot; after the fine test
+//   of each iteration the CTA votes (__syncthreads_or) and stops at the first
+//   iteration in which ANY seed of the target converged (Alg. 4 l.18 break,
+//   P:203/P:309; R26b) — deterministic, no atomics.
+template <int NMAX, bool TEXIT>
+__global__ void __launch_bounds__(256)
 k_pjik(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
        const float* __restrict__ targets, int T, const float* __restrict__ seeds,
        float* __restrict__ theta_out, float* __restrict__ ep_out, float* __restrict__ eo_out,
        int32_t* __restrict__ counts_out, int32_t* __restrict__ iters_out) {
     const int n = rb.n;
     const int used = c.copies * c.K;
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= (long long)T * used) return;
-    const int t = (int)(gid / used);
-    const int b = (int)(gid - (long long)t * used);
+    int t, b;
+    bool active;
+    if (TEXIT) {
+        t = blockIdx.x;
+        b = threadIdx.x;
+        active = b < used;
+    } else {
+        const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        if (gid >= (long long)T * used) return;
+        t = (int)(gid / used);
+        b = (int)(gid - (long long)t * used);
+        active = true;
+    }
     const Target tg = load_target(targets + 7ll * t);
     const uint32_t tid = (uint32_t)(c.tid_offset + t);
     const long long row = (long long)t * c.B + b;
 
     float th[NMAX], tt[NMAX], dth[NMAX];
 #pragma unroll
-    for (int j = 0; j < NMAX; ++j) th[j] = (j < n) ? seeds[row * n + j] : 0.f;
+    for (int j = 0; j < NMAX; ++j) th[j] = (active && j < n) ? seeds[row * n + j] : 0.f;
 
     int cnt[4] = {0, 0, 0, 0};
     float3 Jp[NMAX], Jo[NMAX];   // frames P, z, then Jacobian columns in place
@@ -113,11 +127,20 @@ k_pjik(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     for (k = 0;; ++k) {
         float3 pe;
         Quat qe;
-        fk<NMAX, true>(rb, th, Jp, Jo, pe, qe);
-        r = residual(tg, pe, qe);
-        // Alg. 4 l.18 (R26), checked at iteration start
-        if (r.ep < c.eps_p_fine && r.eo < c.eps_o_fine) break;
+        bool conv = false;
+        if (active) {
+            fk<NMAX, true>(rb, th, Jp, Jo, pe, qe);
+            r = residual(tg, pe, qe);
+            // Alg. 4 l.18 (R26), checked at iteration start
+            conv = r.ep < c.eps_p_fine && r.eo < c.eps_o_fine;
+        }
+        if (TEXIT) {
+            if (__syncthreads_or(conv)) break;
+        } else if (conv) {
+            break;
+        }
         if (k == c.lm_iters) break;
+        if (!active) continue;
 
         // ---- Eq. 7: J columns [z x (P_ee - P_i); z] (prismatic: [z; 0])
 #pragma unroll
@@ -316,6 +339,7 @@ k_pjik(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         }
     }
 
+    if (!active) return;
 #pragma unroll
     for (int j = 0; j < NMAX; ++j)
         if (j < n) theta_out[row * n + j] = th[j];
@@ -332,11 +356,19 @@ template <int NMAX>
 static cudaError_t launch_pjik_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                  const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
                                  int32_t* iters, cudaStream_t s) {
-    const long long total = (long long)T * c.copies * c.K;
-    const int block = 128;
-    const long long grid = (total + block - 1) / block;
-    if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    k_pjik<NMAX><<<(unsigned)grid, block, 0, s>>>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters);
+    const int used = c.copies * c.K;
+    if (c.target_early_exit) {
+        if (used > 256) return cudaErrorInvalidConfiguration;
+        const int block = (used + 31) / 32 * 32;
+        k_pjik<NMAX, true><<<T, block, 0, s>>>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters);
+    } else {
+        const long long total = (long long)T * used;
+        const int block = 128;
+        const long long grid = (total + block - 1) / block;
+        if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+        k_pjik<NMAX, false><<<(unsigned)grid, block, 0, s>>>(rb, c, targets, T, seeds, theta, ep, eo, counts,
+                                                               iters);
+    }
     return cudaGetLastError();
 }
 

@@ -179,8 +179,9 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
 #pragma unroll
             for (int j = 0; j < NMAX; ++j) {
                 if (j < n) {
-                    if (j == jb) th[j] = th[j] + db;
-                    if (j == ja) th[j] = th[j] + da;
+                    // theta + d_eff, re-clamped so rounding never leaves [lo, hi]
+                    if (j == jb) th[j] = clampf(th[j] + db, rb.j[j].lo, rb.j[j].hi);
+                    if (j == ja) th[j] = clampf(th[j] + da, rb.j[j].lo, rb.j[j].hi);
                 }
             }
         } else {

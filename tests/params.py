@@ -15,6 +15,7 @@ DEFAULTS = dict(
     succ_p=1e-3, succ_o=math.pi / 180.0,
     tau_deg=1e-5,                                            # R4
     rng_seed=0, repl_noise_all=0,
+    target_early_exit=1,                                     # R26b
 )
 
 

@@ -451,7 +451,7 @@ def test_poccd_invariants():
 # ---------------------------------------------------------------- P15 PJ-IK special cases
 def test_pjik_zero_error_fixed_point_and_convergence():
     ch = inputs.panda()
-    p = params(B=4, K=2)
+    p = params(B=4, K=2, target_early_exit=0)
     th0 = inputs.halton_configs(ch, 3)
     tgt = oracle.fk(ch, th0).astype(np.float32)
     # seeds on the (fp32-rounded) answer: converged immediately, no steps
@@ -463,6 +463,28 @@ def test_pjik_zero_error_fixed_point_and_convergence():
     r = oracle.pj_ik(ch, p, tgt, seeds)
     assert np.all(r["ep"] < p["eps_p_fine"]) and np.all(r["eo"] < p["eps_o_fine"])
     assert np.all(r["iters"] <= 12)
+
+
+def test_pjik_target_early_exit_is_lockstep_truncation():
+    # R26b: with target_early_exit every seed of a target stops after k* iterations,
+    # k* = the first iteration at which any seed passes the fine test; each seed's
+    # state equals its own per-seed trajectory truncated at k*
+    ch = inputs.fetch_like8()
+    B = 12
+    th0 = inputs.halton_configs(ch, 4)
+    tg = oracle.fk(ch, th0).astype(np.float32)
+    seeds = inputs.near_configs(ch, np.repeat(th0[:, None, :], B, 1), 0.2, seed=3)
+    free = oracle.pj_ik(ch, params(B=B, K=4, target_early_exit=0), tg, seeds)
+    ex = oracle.pj_ik(ch, params(B=B, K=4, target_early_exit=1), tg, seeds)
+    for t in range(4):
+        conv = (free["ep"][t] < 1e-6) & (free["eo"][t] < 1e-5)
+        kstar = free["iters"][t][conv].min() if conv.any() else 128
+        assert np.all(ex["iters"][t] == kstar)
+        trunc = oracle.pj_ik(ch, params(B=B, K=4, target_early_exit=0, lm_iters=int(kstar)), tg[t:t + 1],
+                             seeds[t:t + 1], tid_offset=t)
+        assert np.array_equal(trunc["theta"][0], ex["theta"][t])
+        if conv.any():
+            assert np.any((ex["ep"][t] < 1e-6) & (ex["eo"][t] < 1e-5))
 
 
 # ---------------------------------------------------------------- P16 end to end
