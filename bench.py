@@ -292,7 +292,9 @@ def main():
         for i, k in enumerate(kern):
             kern[k].append(e[i].elapsed_time(e[i + 1]))
         iters_sum = int(o1["iters"].sum().item())
-        pj_iters_sum = int(o2["iters"].sum().item())
+        used = (B // K) * K
+        pj_iters_sum = int(o2["iters"][:, :used].sum().item())
+        kstar = o2["iters"][:, 0].float()
     kmean = {k: statistics.mean(v) for k, v in kern.items()}
     pk = peaks()
     peak_tf, mhz, peak_src = fp32_peak_tflops(pk)
@@ -316,6 +318,10 @@ def main():
                 "k_pjik": {"achieved": pjik_flops / (kmean["k_pjik"] / 1e3) / 1e12,
                            "frac": pjik_flops / (kmean["k_pjik"] / 1e3) / 1e12 / peak_tf},
                 "poccd_mean_iters": iters_sum / seeds_total,
+                "pjik_kstar": {"mean": float(kstar.mean()), "p50": float(kstar.median()),
+                               "p99": float(torch.quantile(kstar, 0.99)), "max": float(kstar.max()),
+                               "frac_at_budget": float((kstar >= cfg.lm_iters).float().mean())},
+                "status_hist": [int((st == i).sum()) for i in range(4)],
                 "pjik_mean_iters": pj_iters_sum / (Tg * (B // K) * K)}
 
     # ---------------- end to end through the C ABI with host buffers

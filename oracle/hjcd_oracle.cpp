@@ -408,6 +408,8 @@ double ccd_position_step(V3 Pj, V3 rj, V3 pee, V3 pt, double tau, double* margin
     double c = dot(scl(vp, 1.0 / norm(vp)), scl(up, 1.0 / norm(up)));
     double mag = std::acos(clampd(c, -1.0, 1.0));
     double sgn = dot(rj, cross(up, vp));
+    /* |dtheta| near pi: the sign (branch cut of the signed angle) is a decision */
+    if (margin) *margin = std::min(*margin, PI - mag);
     return (sgn > 0) ? mag : (sgn < 0 ? -mag : 0.0);
 }
 
@@ -451,6 +453,8 @@ SeedOut po_ccd_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, u
         double phi; V3 ahat;
         angle_axis(tgt.q, F.qee, &phi, &ahat);
         double dk = delta_k(c, k);
+        /* the w >= 0 canonicalisation of q_err flips a (R1/R2) when w crosses 0 */
+        if (phi > 0) so.margin = std::min(so.margin, std::fabs(std::cos(phi / 2.0)));
         std::vector<double> sp(n), sop(n), dp(n), dor(n);
         for (int j = 0; j < n; ++j) {
             int ent = rb.dof_entry[j];
@@ -754,6 +758,8 @@ bool pj_ik_check(const Robot& rb, const OracleConfig& c, const Target& tgt,
     bool cp = e.ep < c.eps_p_fine, co = e.eo < c.eps_o_fine;
     po.margin = std::min(po.margin, margin_and(cp, rel_gap(e.ep, c.eps_p_fine, 0), co,
                                                rel_gap(e.eo, c.eps_o_fine, 0)));
+    /* omega's direction flips where the canonical q_err has w = 0 (|omega| = pi) */
+    po.margin = std::min(po.margin, std::fabs(std::cos(e.eo / 2.0)));
     po.ep = e.ep;
     po.eo = e.eo;
     return cp && co;

@@ -104,14 +104,17 @@ __device__ __forceinline__ Quat quat_from_rot(const float R[9]) {
 // T = F_1 Rz(th_1) F_2 Rz(th_2) ... F_n Rz(th_n) EE  (prismatic: Tz).
 // FRAMES: P[j] = joint origin, Z[j] = joint axis (world), before joint motion
 // (identical after it: rotation about z fixes the axis and the origin).
-template <int NMAX, bool FRAMES>
+// EXACT: the chain has exactly NMAX DoF (no per-joint guard).  FAST: joint
+// sincos on the SFU (__sincosf, |err| <~ 5e-7 rad on the joint ranges): used by
+// the coarse stage only (K5); the polish stage uses accurate sincosf.
+template <int NMAX, bool FRAMES, bool EXACT = false, bool FAST = false>
 __device__ __forceinline__ void fk(const DevRobot& rb, const float (&th)[NMAX], float3 (&P)[NMAX],
                                    float3 (&Z)[NMAX], float3& pe, Quat& qe) {
     float R[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
     float tx = 0.f, ty = 0.f, tz = 0.f;
 #pragma unroll
     for (int j = 0; j < NMAX; ++j) {
-        if (j < rb.n) {
+        if (EXACT || j < rb.n) {
             const DevJoint& J = rb.j[j];
             tx += R[0] * J.t[0] + R[1] * J.t[1] + R[2] * J.t[2];
             ty += R[3] * J.t[0] + R[4] * J.t[1] + R[5] * J.t[2];
@@ -128,7 +131,8 @@ __device__ __forceinline__ void fk(const DevRobot& rb, const float (&th)[NMAX], 
             }
             if (J.type == HJCD_REVOLUTE) {
                 float s, c;
-                sincosf(th[j], &s, &c);
+                if (FAST) __sincosf(th[j], &s, &c);
+                else sincosf(th[j], &s, &c);
 #pragma unroll
                 for (int r = 0; r < 3; ++r) {
                     float a = N[3 * r], b = N[3 * r + 1];
@@ -156,6 +160,27 @@ __device__ __forceinline__ void fk(const DevRobot& rb, const float (&th)[NMAX], 
             E[3 * r + cc] = R[3 * r] * rb.eeR[cc] + R[3 * r + 1] * rb.eeR[3 + cc] + R[3 * r + 2] * rb.eeR[6 + cc];
     pe = f3(tx, ty, tz);
     qe = quat_from_rot(E);
+}
+
+// atan2 on [-pi, pi] with |err| <= 3.3e-7 rad (fp32): odd minimax polynomial
+// of degree 15 for atan on [0, 1] + octant reduction (K5)
+__device__ __forceinline__ float fast_atan2f(float y, float x) {
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    const float r = mx > 0.f ? __fdividef(mn, mx) : 0.f;
+    const float s = r * r;
+    float p = -0.00405456f;
+    p = fmaf(p, s, 0.02186293f);
+    p = fmaf(p, s, -0.05591229f);
+    p = fmaf(p, s, 0.09642195f);
+    p = fmaf(p, s, -0.13908629f);
+    p = fmaf(p, s, 0.19946566f);
+    p = fmaf(p, s, -0.3332986f);
+    p = fmaf(p, s, 0.99999934f);
+    float a = p * r;
+    a = (ay > ax) ? 1.57079637f - a : a;
+    a = (x < 0.f) ? 3.14159274f - a : a;
+    return copysignf(a, y);
 }
 
 // ---------------------------------------------------------------- targets
@@ -212,18 +237,18 @@ __device__ __forceinline__ void normals4(uint4 r, float g[4]) {
 }
 
 // theta <- clamp(theta + sigma * N(0, I)), stream (tid, sid, purpose, iter)
-template <int NMAX>
+template <int NMAX, bool EXACT = false>
 __device__ __forceinline__ void perturb(const DevRobot& rb, const DevCfg& c, float (&th)[NMAX], float sigma,
                                         uint32_t tid, uint32_t sid, uint32_t purpose, uint32_t iter) {
 #pragma unroll
     for (int blk = 0; blk < (NMAX + 3) / 4; ++blk) {
-        if (4 * blk < rb.n) {
+        if (EXACT || 4 * blk < rb.n) {
             float g[4];
             normals4(draw(c, tid, sid, purpose, iter, blk), g);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 int j = 4 * blk + e;
-                if (j < NMAX && j < rb.n) th[j] = clampf(th[j] + sigma * g[e], rb.j[j].lo, rb.j[j].hi);
+                if (j < NMAX && (EXACT || j < rb.n)) th[j] = clampf(th[j] + sigma * g[e], rb.j[j].lo, rb.j[j].hi);
             }
         }
     }

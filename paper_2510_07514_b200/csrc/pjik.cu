@@ -86,6 +86,153 @@ __device__ __forceinline__ Resid eval_at(const DevRobot& rb, const Target& tg, c
     return residual(tg, pe, qe);
 }
 
+// ---- LM direction (Eq. 12 via push-through, K4): A = W G W + lambda I,
+//      G_ik = sum_j J_ij J_kj / D_j; y = A^-1 W rho; dth_j = -(sum_i J_ij W_i y_i) / D_j,
+//      then the element-wise trust-region clamp (Alg. 4 l.6, R21)
+template <int NMAX>
+__device__ __forceinline__ bool lm_direction(const DevRobot& rb, const DevCfg& c, const float3 (&Jp)[NMAX],
+                                             const float3 (&Jo)[NMAX], const float (&invD)[NMAX],
+                                             const float (&W)[6], const float (&rho)[6], float (&dth)[NMAX]) {
+    const int n = rb.n;
+    float A[21];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int kk = 0; kk <= i; ++kk) {
+            float s = 0.f;
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j)
+                if (j < n) s += jrow(Jp[j], Jo[j], i) * jrow(Jp[j], Jo[j], kk) * invD[j];
+            A[i * (i + 1) / 2 + kk] = W[i] * W[kk] * s + (i == kk ? c.lambda : 0.f);
+        }
+    float y[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) y[i] = W[i] * rho[i];
+    if (!chol6_solve(A, y)) return false;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) y[i] *= W[i];
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) {
+        if (j < n) {
+            const float s = Jp[j].x * y[0] + Jp[j].y * y[1] + Jp[j].z * y[2] + Jo[j].x * y[3] +
+                            Jo[j].y * y[4] + Jo[j].z * y[5];
+            dth[j] = clampf(-s * invD[j], -c.R, c.R);
+        }
+    }
+    return true;
+}
+
+// ---- dogleg direction (Eqs. 14-15, R23): GD = -alpha_c J^T rho (Cauchy),
+//      GN = -J^T (J J^T + d_floor I)^-1 rho, smallest tau in [0,1] with |dth(tau)| <= R
+template <int NMAX>
+__device__ __forceinline__ bool dogleg_direction(const DevRobot& rb, const DevCfg& c, const float3 (&Jp)[NMAX],
+                                                 const float3 (&Jo)[NMAX], const float (&rho)[6],
+                                                 float (&dth)[NMAX], float (&gn)[NMAX]) {
+    const int n = rb.n;
+    float gg = 0.f;
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) {
+        if (j < n) {
+            dth[j] = Jp[j].x * rho[0] + Jp[j].y * rho[1] + Jp[j].z * rho[2] + Jo[j].x * rho[3] +
+                     Jo[j].y * rho[4] + Jo[j].z * rho[5];   // g0 = J^T rho
+            gg += dth[j] * dth[j];
+        }
+    }
+    float jg2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j)
+            if (j < n) s += jrow(Jp[j], Jo[j], i) * dth[j];
+        jg2 += s * s;
+    }
+    if (!(gg > 0.f) || !(jg2 > 0.f)) return false;
+    const float alpha_c = gg / jg2;
+    float A[21];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int kk = 0; kk <= i; ++kk) {
+            float s = 0.f;
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j)
+                if (j < n) s += jrow(Jp[j], Jo[j], i) * jrow(Jp[j], Jo[j], kk);
+            A[i * (i + 1) / 2 + kk] = s + (i == kk ? c.d_floor : 0.f);
+        }
+    float y[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) y[i] = rho[i];
+    if (!chol6_solve(A, y)) return false;
+    float ngn2 = 0.f, ngd2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) {
+        if (j < n) {
+            gn[j] = -(Jp[j].x * y[0] + Jp[j].y * y[1] + Jp[j].z * y[2] + Jo[j].x * y[3] + Jo[j].y * y[4] +
+                      Jo[j].z * y[5]);
+            dth[j] = -alpha_c * dth[j];   // GD
+            ngn2 += gn[j] * gn[j];
+            ngd2 += dth[j] * dth[j];
+        }
+    }
+    const float R2 = c.R * c.R;
+    float wgd, wgn;   // step = wgd * GD + wgn * GN
+    if (ngn2 <= R2) {
+        wgd = 0.f; wgn = 1.f;
+    } else {
+        float qa = 0.f, qb = 0.f;
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) {
+            if (j < n) {
+                const float d = dth[j] - gn[j];
+                qa += d * d;
+                qb += 2.f * gn[j] * d;
+            }
+        }
+        const float qc = ngn2 - R2;
+        const float disc = qb * qb - 4.f * qa * qc;
+        float tau = -1.f;
+        if (qa > 0.f && disc >= 0.f) {
+            const float sd = sqrtf(disc);
+            tau = (qb < 0.f) ? (2.f * qc) / (-qb + sd) : (-qb - sd) / (2.f * qa);   // smaller root
+        }
+        if (tau >= 0.f && tau <= 1.f) { wgd = tau; wgn = 1.f - tau; }
+        else { wgd = c.R / sqrtf(ngd2); wgn = 0.f; }
+    }
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j)
+        if (j < n) dth[j] = wgd * dth[j] + wgn * gn[j];
+    return true;
+}
+
+// ---- single-coordinate direction (Eq. 16, R24): i* = argmax |g_i|, g = J^T W^2 rho,
+//      step -sign(g_i*) min(|g_i*|, R) on i* only
+template <int NMAX>
+__device__ __forceinline__ bool single_coord_direction(const DevRobot& rb, const DevCfg& c,
+                                                       const float3 (&Jp)[NMAX], const float3 (&Jo)[NMAX],
+                                                       const float (&W)[6], const float (&rho)[6],
+                                                       float (&dth)[NMAX]) {
+    const int n = rb.n;
+    float wr[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) wr[i] = W[i] * W[i] * rho[i];
+    int ist = 0;
+    float gbest = 0.f, gabs = -1.f;
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) {
+        if (j < n) {
+            const float g = Jp[j].x * wr[0] + Jp[j].y * wr[1] + Jp[j].z * wr[2] + Jo[j].x * wr[3] +
+                            Jo[j].y * wr[4] + Jo[j].z * wr[5];
+            if (fabsf(g) > gabs) { gabs = fabsf(g); gbest = g; ist = j; }
+        }
+    }
+    if (gbest == 0.f) return false;
+    const float step = (gbest > 0.f) ? -fminf(gabs, c.R) : fminf(gabs, c.R);
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) dth[j] = (j == ist) ? step : 0.f;
+    return true;
+}
+
 // TEXIT = false: one thread per polish seed anywhere in the grid, per-seed break.
 // TEXIT = true : one CTA per target, thread b = polish slot; after the fine test
 //   of each iteration the CTA votes (__syncthreads_or) and stops at the first
@@ -171,163 +318,48 @@ k_pjik(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
             for (int i = 0; i < 6; ++i) W[i] = (i < 3 ? c.w_p : c.w_o) / (1.f + sqrtf(rn[i]));
         }
         const float c0 = cost_w(W, r.rho);
+        float n0 = 0.f;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) n0 += r.rho[i] * r.rho[i];
 
+        // Fallback cascade of Alg. 4 (l.3-17) as a state machine with ONE trial
+        // evaluation site: phase 0 = LM + line search (Eq. 12-13), 1 = dogleg
+        // (Eqs. 14-15), 2 = single coordinate + line search (Eq. 16), 3 = perturb.
         bool accepted = false;
-        // ---- LM step (Eq. 12 via push-through): A = W G W + lambda I,
-        //      G_ik = sum_j J_ij J_kj / D_j; y = A^-1 W rho; dth_j = -(sum_i J_ij W_i y_i) / D_j
-        {
-            float A[21];
-#pragma unroll
-            for (int i = 0; i < 6; ++i)
-#pragma unroll
-                for (int kk = 0; kk <= i; ++kk) {
-                    float s = 0.f;
-#pragma unroll
-                    for (int j = 0; j < NMAX; ++j)
-                        if (j < n) s += jrow(Jp[j], Jo[j], i) * jrow(Jp[j], Jo[j], kk) * invD[j];
-                    A[i * (i + 1) / 2 + kk] = W[i] * W[kk] * s + (i == kk ? c.lambda : 0.f);
+        int phase = 0;
+        bool have = lm_direction<NMAX>(rb, c, Jp, Jo, invD, W, r.rho, dth);
+        if (!have) phase = 1;
+        int a = 0;
+        float alpha = 1.f;
+        for (;;) {
+            if (!have) {
+                // prepare the direction of the current phase
+                if (phase == 1) have = dogleg_direction<NMAX>(rb, c, Jp, Jo, r.rho, dth, tt);
+                else if (phase == 2) have = single_coord_direction<NMAX>(rb, c, Jp, Jo, W, r.rho, dth);
+                if (!have) {
+                    if (++phase >= 3) break;
+                    continue;
                 }
-            float y[6];
-#pragma unroll
-            for (int i = 0; i < 6; ++i) y[i] = W[i] * r.rho[i];
-            if (chol6_solve(A, y)) {
-#pragma unroll
-                for (int i = 0; i < 6; ++i) y[i] *= W[i];
-#pragma unroll
-                for (int j = 0; j < NMAX; ++j) {
-                    if (j < n) {
-                        float s = Jp[j].x * y[0] + Jp[j].y * y[1] + Jp[j].z * y[2] +
-                                  Jo[j].x * y[3] + Jo[j].y * y[4] + Jo[j].z * y[5];
-                        dth[j] = clampf(-s * invD[j], -c.R, c.R);   // Alg. 4 l.6 (R21)
-                    }
-                }
-                // ---- Eq. 13 line search (R22): first alpha with c_W < c0
-                float alpha = 1.f;
-                for (int a = 0; a <= c.A; ++a) {
-#pragma unroll
-                    for (int j = 0; j < NMAX; ++j)
-                        if (j < n) tt[j] = clampf(th[j] + alpha * dth[j], rb.j[j].lo, rb.j[j].hi);
-                    const Resid rt = eval_at<NMAX>(rb, tg, tt);
-                    if (cost_w(W, rt.rho) < c0) { accepted = true; break; }
-                    alpha *= c.inv_beta;
-                }
-                if (accepted) cnt[0]++;
+                a = 0;
+                alpha = 1.f;
             }
-        }
-        // ---- dogleg (Eqs. 14-15, R23): GD = -alpha_c J^T rho, GN = -J^T (J J^T + d I)^-1 rho
-        if (!accepted) {
-            float gg = 0.f;
 #pragma unroll
-            for (int j = 0; j < NMAX; ++j) {
-                if (j < n) {
-                    dth[j] = Jp[j].x * r.rho[0] + Jp[j].y * r.rho[1] + Jp[j].z * r.rho[2] +
-                             Jo[j].x * r.rho[3] + Jo[j].y * r.rho[4] + Jo[j].z * r.rho[5];   // g0
-                    gg += dth[j] * dth[j];
-                }
+            for (int j = 0; j < NMAX; ++j)
+                if (j < n) tt[j] = clampf(th[j] + alpha * dth[j], rb.j[j].lo, rb.j[j].hi);
+            const Resid rt = eval_at<NMAX>(rb, tg, tt);
+            bool ok;
+            if (phase == 1) {   // dogleg acceptance on the unweighted |rho| (R23)
+                float nt = 0.f;
+#pragma unroll
+                for (int i = 0; i < 6; ++i) nt += rt.rho[i] * rt.rho[i];
+                ok = nt < n0;
+            } else {            // Eq. 13: c_W(trial) < c_W(theta), W frozen (R22)
+                ok = cost_w(W, rt.rho) < c0;
             }
-            float jg2 = 0.f;
-#pragma unroll
-            for (int i = 0; i < 6; ++i) {
-                float s = 0.f;
-#pragma unroll
-                for (int j = 0; j < NMAX; ++j)
-                    if (j < n) s += jrow(Jp[j], Jo[j], i) * dth[j];
-                jg2 += s * s;
-            }
-            if (gg > 0.f && jg2 > 0.f) {
-                const float alpha_c = gg / jg2;
-                float A[21];
-#pragma unroll
-                for (int i = 0; i < 6; ++i)
-#pragma unroll
-                    for (int kk = 0; kk <= i; ++kk) {
-                        float s = 0.f;
-#pragma unroll
-                        for (int j = 0; j < NMAX; ++j)
-                            if (j < n) s += jrow(Jp[j], Jo[j], i) * jrow(Jp[j], Jo[j], kk);
-                        A[i * (i + 1) / 2 + kk] = s + (i == kk ? c.d_floor : 0.f);
-                    }
-                float y[6];
-#pragma unroll
-                for (int i = 0; i < 6; ++i) y[i] = r.rho[i];
-                if (chol6_solve(A, y)) {
-                    // gd in dth (scaled g0), gn in tt temporarily
-                    float ngn2 = 0.f, ngd2 = 0.f;
-#pragma unroll
-                    for (int j = 0; j < NMAX; ++j) {
-                        if (j < n) {
-                            tt[j] = -(Jp[j].x * y[0] + Jp[j].y * y[1] + Jp[j].z * y[2] +
-                                      Jo[j].x * y[3] + Jo[j].y * y[4] + Jo[j].z * y[5]);
-                            dth[j] = -alpha_c * dth[j];
-                            ngn2 += tt[j] * tt[j];
-                            ngd2 += dth[j] * dth[j];
-                        }
-                    }
-                    const float R2 = c.R * c.R;
-                    float wgd, wgn;   // step = wgd * gd + wgn * gn
-                    if (ngn2 <= R2) {
-                        wgd = 0.f; wgn = 1.f;
-                    } else {
-                        float qa = 0.f, qb = 0.f;
-#pragma unroll
-                        for (int j = 0; j < NMAX; ++j) {
-                            if (j < n) {
-                                const float d = dth[j] - tt[j];
-                                qa += d * d;
-                                qb += 2.f * tt[j] * d;
-                            }
-                        }
-                        const float qc = ngn2 - R2;
-                        const float disc = qb * qb - 4.f * qa * qc;
-                        float tau = -1.f;
-                        if (qa > 0.f && disc >= 0.f) {
-                            const float sd = sqrtf(disc);
-                            // smaller root, cancellation-free form
-                            tau = (qb < 0.f) ? (2.f * qc) / (-qb + sd) : (-qb - sd) / (2.f * qa);
-                        }
-                        if (tau >= 0.f && tau <= 1.f) { wgd = tau; wgn = 1.f - tau; }
-                        else { wgd = c.R / sqrtf(ngd2); wgn = 0.f; }
-                    }
-#pragma unroll
-                    for (int j = 0; j < NMAX; ++j)
-                        if (j < n) dth[j] = wgd * dth[j] + wgn * tt[j];
-#pragma unroll
-                    for (int j = 0; j < NMAX; ++j)
-                        if (j < n) tt[j] = clampf(th[j] + dth[j], rb.j[j].lo, rb.j[j].hi);
-                    const Resid rt = eval_at<NMAX>(rb, tg, tt);
-                    float n0 = 0.f, nt = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 6; ++i) { n0 += r.rho[i] * r.rho[i]; nt += rt.rho[i] * rt.rho[i]; }
-                    if (nt < n0) { accepted = true; cnt[1]++; }   // unweighted |rho| (R23)
-                }
-            }
-        }
-        // ---- single coordinate (Eq. 16, R24): i* = argmax |g_i|, g = J^T W^2 rho
-        if (!accepted) {
-            int ist = 0;
-            float gbest = 0.f, gabs = -1.f;
-#pragma unroll
-            for (int j = 0; j < NMAX; ++j) {
-                if (j < n) {
-                    float g = 0.f;
-#pragma unroll
-                    for (int i = 0; i < 6; ++i) g += jrow(Jp[j], Jo[j], i) * W[i] * W[i] * r.rho[i];
-                    if (fabsf(g) > gabs) { gabs = fabsf(g); gbest = g; ist = j; }
-                }
-            }
-            if (gbest != 0.f) {
-                const float step = (gbest > 0.f) ? -fminf(gabs, c.R) : fminf(gabs, c.R);
-                float alpha = 1.f;
-                for (int a = 0; a <= c.A; ++a) {
-#pragma unroll
-                    for (int j = 0; j < NMAX; ++j)
-                        if (j < n) tt[j] = (j == ist) ? clampf(th[j] + alpha * step, rb.j[j].lo, rb.j[j].hi) : th[j];
-                    const Resid rt = eval_at<NMAX>(rb, tg, tt);
-                    if (cost_w(W, rt.rho) < c0) { accepted = true; break; }
-                    alpha *= c.inv_beta;
-                }
-                if (accepted) cnt[2]++;
-            }
+            if (ok) { accepted = true; cnt[phase]++; break; }
+            if (phase != 1 && a < c.A) { ++a; alpha *= c.inv_beta; continue; }
+            have = false;
+            if (++phase >= 3) break;
         }
         if (accepted) {
 #pragma unroll

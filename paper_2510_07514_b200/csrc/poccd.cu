@@ -14,7 +14,7 @@
 
 namespace hjcd {
 
-template <int NMAX>
+template <int NMAX, bool EXACT>
 __global__ void __launch_bounds__(128)
 k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float* __restrict__ targets, int T, const float* __restrict__ seeds,
@@ -34,17 +34,17 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     if (seeds) {
 #pragma unroll
         for (int j = 0; j < NMAX; ++j)
-            if (j < n) th[j] = seeds[((long long)t * n + j) * M + m];
+            if (EXACT || j < n) th[j] = seeds[((long long)t * n + j) * M + m];
     } else {
 #pragma unroll
         for (int blk = 0; blk < (NMAX + 3) / 4; ++blk) {
-            if (4 * blk < n) {
+            if (EXACT || 4 * blk < n) {
                 uint4 r = draw(c, tid, (uint32_t)m, P_INIT, 0u, (uint32_t)blk);
                 uint32_t x[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     int j = 4 * blk + e;
-                    if (j < NMAX && j < n) {
+                    if (j < NMAX && (EXACT || j < n)) {
                         float lo = rb.j[j].lo, hi = rb.j[j].hi;
                         th[j] = __fmaf_rn(__fsub_rn(hi, lo), u01(x[e]), lo);
                     }
@@ -57,14 +57,15 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     float3 pe;
     Quat qe;
     float ep = 0.f, eo = 0.f;
+    float rho_k = 1.f;   // delta_rho^k, by repeated multiplication (R5)
     int k;
-    for (k = 0;; ++k) {
-        fk<NMAX, true>(rb, th, P, Z, pe, qe);
+    for (k = 0;; ++k, rho_k *= c.delta_rho) {
+        fk<NMAX, true, EXACT, true>(rb, th, P, Z, pe, qe);
         const float3 rp = tg.p - pe;                   // r_p (Eq. 4)
         const Quat qr = quat_err(tg.q, qe);            // q_err (Eq. 5), w >= 0
         const float sv = sqrtf(qr.x * qr.x + qr.y * qr.y + qr.z * qr.z);
         ep = sqrtf(dot3(rp, rp));
-        eo = omega_norm(sv, qr.w);
+        eo = 2.f * fast_atan2f(sv, qr.w);              // |omega|
         // Alg. 3 l.14: coarse test (R12), checked at iteration start
         if (ep < c.eps_p_coarse && eo < c.eps_o_coarse) break;
         if (k == c.ccd_iters) break;
@@ -73,7 +74,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float phi = eo;
         const float inv_sv = sv > 0.f ? 1.f / sv : 0.f;
         const float3 ahat = f3(qr.x * inv_sv, qr.y * inv_sv, qr.z * inv_sv);
-        const float dk = fmaxf(c.delta_min, c.delta0 * powf(c.delta_rho, (float)k));   // R5
+        const float dphi = phi > 0.f ? fmaxf(c.delta_min, c.delta0 * rho_k) * phi : 0.f;   // delta(k) phi
         const float tau2 = c.tau_deg * c.tau_deg;
 
         // ---- Alg. 3 l.6-9: per-joint candidates, scored, greedy argmin
@@ -84,35 +85,37 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         int typ_p = HJCD_REVOLUTE;
 #pragma unroll
         for (int j = 0; j < NMAX; ++j) {
-            if (j < n) {
+            if (EXACT || j < n) {
                 const DevJoint& J = rb.j[j];
                 const float3 z = Z[j];
                 float dp, sp, dor, so;
                 if (J.type == HJCD_REVOLUTE) {
                     // Eqs. 8-9 (R3): signed angle between the projections of
-                    // P_ee - P_j and P_t - P_j on the plane normal to z_j
+                    // u = P_ee - P_j and v = P_t - P_j on the plane normal to z_j;
+                    // z.(u_p x v_p) = (z x u).v_p
                     const float3 u = pe - P[j];
                     const float3 v = tg.p - P[j];
                     const float3 up = u - dot3(u, z) * z;
                     const float3 vp = v - dot3(v, z) * z;
+                    const float3 zxu = cross3(z, u);
                     float step = 0.f;
                     if (dot3(up, up) >= tau2 && dot3(vp, vp) >= tau2)   // R4
-                        step = atan2f(dot3(z, cross3(up, vp)), dot3(up, vp));
+                        step = fast_atan2f(dot3(zxu, vp), dot3(up, vp));
                     dp = clampf(th[j] + step, J.lo, J.hi) - th[j];     // R7
-                    // score: r_p' = r_p + (1 - cos d) u_perp - sin d (z x u)
+                    // score (K2): r_p' = r_p + (1 - cos d) u_perp - sin d (z x u)
                     float s2, c2;
-                    sincosf(0.5f * dp, &s2, &c2);
+                    __sincosf(0.5f * dp, &s2, &c2);
+                    if (dp == 0.f) { s2 = 0.f; c2 = 1.f; }
                     const float sn = 2.f * s2 * c2, omc = 2.f * s2 * s2;
-                    const float3 zxu = cross3(z, u);
                     const float3 r2 = rp + omc * up - sn * zxu;
                     sp = dot3(r2, r2);
                     // Eq. 11 (R5): delta(k) sgn(a . z_j) phi, sgn(0) = 0
                     const float az = dot3(ahat, z);
                     const float sg = az > 0.f ? 1.f : (az < 0.f ? -1.f : 0.f);
-                    const float so_step = phi > 0.f ? dk * sg * phi : 0.f;
-                    dor = clampf(th[j] + so_step, J.lo, J.hi) - th[j];
-                    // score: |v'|^2 of q_err (x) q(z, -d) (monotone in |omega'|)
-                    sincosf(0.5f * dor, &s2, &c2);
+                    dor = clampf(th[j] + sg * dphi, J.lo, J.hi) - th[j];
+                    // score (K2): |v'|^2 of q_err (x) q(z, -d), monotone in |omega'|
+                    __sincosf(0.5f * dor, &s2, &c2);
+                    if (dor == 0.f) { s2 = 0.f; c2 = 1.f; }
                     const Quat q2 = qerr_rotate(qr, z, c2, s2);
                     so = q2.x * q2.x + q2.y * q2.y + q2.z * q2.z;
                 } else {
@@ -150,7 +153,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         {
             if (tb == HJCD_REVOLUTE) {
                 float s2, c2;
-                sincosf(0.5f * db, &s2, &c2);
+                __sincosf(0.5f * db, &s2, &c2);
                 const float3 u = p2 - Pb;
                 const float3 up = u - dot3(u, Zb) * Zb;
                 p2 = p2 - (2.f * s2 * s2) * up + (2.f * s2 * c2) * cross3(Zb, u);
@@ -161,7 +164,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
             if (ja >= 0) {
                 if (ta == HJCD_REVOLUTE) {
                     float s2, c2;
-                    sincosf(0.5f * da, &s2, &c2);
+                    __sincosf(0.5f * da, &s2, &c2);
                     const float3 u = p2 - Pa;
                     const float3 up = u - dot3(u, Za) * Za;
                     p2 = p2 - (2.f * s2 * s2) * up + (2.f * s2 * c2) * cross3(Za, u);
@@ -173,25 +176,25 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         }
         const float3 rh = tg.p - p2;
         const float ep_h = sqrtf(dot3(rh, rh));
-        const float eo_h = omega_norm(sqrtf(q2.x * q2.x + q2.y * q2.y + q2.z * q2.z), q2.w);
+        const float eo_h = 2.f * fast_atan2f(sqrtf(q2.x * q2.x + q2.y * q2.y + q2.z * q2.z), fabsf(q2.w));
         // ---- Alg. 3 l.11-13 (R10): accept on an improvement > gamma in either space
         if ((ep - ep_h) > c.gamma || (eo - eo_h) > c.gamma) {
 #pragma unroll
             for (int j = 0; j < NMAX; ++j) {
-                if (j < n) {
+                if (EXACT || j < n) {
                     // theta + d_eff, re-clamped so rounding never leaves [lo, hi]
                     if (j == jb) th[j] = clampf(th[j] + db, rb.j[j].lo, rb.j[j].hi);
                     if (j == ja) th[j] = clampf(th[j] + da, rb.j[j].lo, rb.j[j].hi);
                 }
             }
         } else {
-            perturb<NMAX>(rb, c, th, c.sigma_ccd, tid, (uint32_t)m, P_PERTURB, (uint32_t)k);   // R11
+            perturb<NMAX, EXACT>(rb, c, th, c.sigma_ccd, tid, (uint32_t)m, P_PERTURB, (uint32_t)k);   // R11
         }
     }
 
 #pragma unroll
     for (int j = 0; j < NMAX; ++j)
-        if (j < n) theta_out[((long long)t * n + j) * M + m] = th[j];
+        if (EXACT || j < n) theta_out[((long long)t * n + j) * M + m] = th[j];
     const long long o = (long long)t * M + m;
     cost_out[o] = c.w_p * c.w_p * ep * ep + c.w_o * c.w_o * eo * eo;   // R14
     if (ep_out) ep_out[o] = ep;
@@ -199,7 +202,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     if (iters_out) iters_out[o] = k;
 }
 
-template <int NMAX>
+template <int NMAX, bool EXACT>
 static cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                   const float* seeds, float* theta, float* cost, float* ep, float* eo,
                                   int32_t* iters, cudaStream_t s) {
@@ -207,16 +210,22 @@ static cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const flo
     const int block = 128;
     const long long grid = (total + block - 1) / block;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    k_poccd<NMAX><<<(unsigned)grid, block, 0, s>>>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters);
+    k_poccd<NMAX, EXACT><<<(unsigned)grid, block, 0, s>>>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters);
     return cudaGetLastError();
 }
 
 cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                          const float* seeds, float* theta, float* cost, float* ep, float* eo,
                          int32_t* iters, cudaStream_t s) {
-    if (rb.n <= 8) return launch_poccd_t<8>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-    if (rb.n <= 16) return launch_poccd_t<16>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-    return launch_poccd_t<32>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+    switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
+        case 7: return launch_poccd_t<7, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+        case 8: return launch_poccd_t<8, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+        case 14: return launch_poccd_t<14, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+        default: break;
+    }
+    if (rb.n <= 8) return launch_poccd_t<8, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+    if (rb.n <= 16) return launch_poccd_t<16, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+    return launch_poccd_t<32, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
 }
 
 }  // namespace hjcd
