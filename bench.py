@@ -271,30 +271,32 @@ def main():
     st_np = st.cpu().numpy()
     succ = float(np.mean(st_np <= 1))
 
-    # ---------------- per-kernel breakdown (same kernels, staged entry points)
+    # ---------------- per-kernel breakdown (same kernels, staged entry points;
+    # each stage timed alone: flush, sync, event, launch, event)
     kern = {"k_poccd": [], "k_select_replicate": [], "k_pjik": [], "k_select_best": []}
-    iters_sum = None
-    pj_iters_sum = None
     nb = max(3, min(args.steps, 10))
-    for s in range(nb):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
-        flush.fill_(s & 0xFF)
-        e[0].record(stream)
-        o1 = hjcd.poccd(robot, cfg, targets)
-        e[1].record(stream)
-        seeds, _ = hjcd.select_replicate(robot, cfg, o1["cost"], o1["theta"])
-        e[2].record(stream)
-        o2 = hjcd.pjik(robot, cfg, targets, seeds)
-        e[3].record(stream)
-        hjcd.select_best(robot, cfg, targets, o2["theta"], o2["ep"], o2["eo"])
-        e[4].record(stream)
+
+    def timed(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.fill_(7)
         torch.cuda.synchronize()
-        for i, k in enumerate(kern):
-            kern[k].append(e[i].elapsed_time(e[i + 1]))
-        iters_sum = int(o1["iters"].sum().item())
-        used = (B // K) * K
-        pj_iters_sum = int(o2["iters"][:, :used].sum().item())
-        kstar = o2["iters"][:, 0].float()
+        e0.record(stream)
+        r = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return r, e0.elapsed_time(e1)
+
+    for s in range(nb):
+        o1, t1 = timed(lambda: hjcd.poccd(robot, cfg, targets))
+        (seeds, _), t2 = timed(lambda: hjcd.select_replicate(robot, cfg, o1["cost"], o1["theta"]))
+        o2, t3 = timed(lambda: hjcd.pjik(robot, cfg, targets, seeds))
+        _, t4 = timed(lambda: hjcd.select_best(robot, cfg, targets, o2["theta"], o2["ep"], o2["eo"]))
+        for k, v in zip(kern, (t1, t2, t3, t4)):
+            kern[k].append(v)
+    iters_sum = int(o1["iters"].sum().item())
+    used = (B // K) * K
+    pj_iters_sum = int(o2["iters"][:, :used].sum().item())
+    kstar = o2["iters"][:, 0].float()
     kmean = {k: statistics.mean(v) for k, v in kern.items()}
     pk = peaks()
     peak_tf, mhz, peak_src = fp32_peak_tflops(pk)

@@ -182,8 +182,9 @@ hjcd_status hjcd_pjik(const hjcd_robot* r, const hjcd_config* c, const float* ta
                       const float* seeds, float* theta, float* pos_err, float* ori_err,
                       int32_t* step_counts, int32_t* iters, hjcd_stream_t stream);
 
-/* Best-of-B selection (Alg. 2 l.9-10, R27): argmin_b w_p^2 pe^2 + w_o^2 oe^2, ties
- * -> lowest b; writes q_out/pos_err/ori_err/status as hjcd_solve does. */
+/* Best-of-B selection (Alg. 2 l.9-10, R27): fine-converged seeds first, then
+ * argmin_b w_p^2 pe^2 + w_o^2 oe^2, ties -> lowest b; writes
+ * q_out/pos_err/ori_err/status as hjcd_solve does. */
 hjcd_status hjcd_select_best(const hjcd_robot* r, const hjcd_config* c, const float* targets,
                              int32_t T, const float* theta, const float* pos_err_all,
                              const float* ori_err_all, float* q_out, float* pos_err,

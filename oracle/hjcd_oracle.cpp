@@ -1133,12 +1133,19 @@ void oracle_solve(const OracleRobot* r, const OracleConfig* c, const float* targ
         } else {
             for (int b = 0; b < used; ++b) po[b] = pj_ik_seed(rb, *c, tgt, tid, (uint32_t)b, th2[b]);
         }
+        /* R27: theta* = argmin over (not fine-converged, c), ties -> lowest slot:
+         * a seed that passed Alg. 4 l.18 is the answer the break returns */
+        int btier = 2;
         double best = INF;
         double bep = INF, beo = INF;
         std::vector<double> bth(n, 0.0);
         for (int b = 0; b < used; ++b) {
+            int tier = (po[b].ep < c->eps_p_fine && po[b].eo < c->eps_o_fine) ? 0 : 1;
             double cb = rank_cost(*c, po[b].ep, po[b].eo);
-            if (cb < best) { best = cb; bep = po[b].ep; beo = po[b].eo; bth = th2[b]; }
+            if (!(cb >= 0)) cb = INF;
+            if (tier < btier || (tier == btier && cb < best)) {
+                btier = tier; best = cb; bep = po[b].ep; beo = po[b].eo; bth = th2[b];
+            }
         }
         for (int j = 0; j < n; ++j) q_out[(size_t)t * n + j] = bth[j];
         pos_err[t] = bep;

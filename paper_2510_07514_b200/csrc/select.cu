@@ -4,8 +4,9 @@
 //     One CTA per target; the M keys (order-preserving cost bits << 32 | index)
 //     are bitonic-sorted in shared memory, which yields exactly the K rounds of
 //     argmin-and-remove of Alg. 2 (ties -> lower index).
-//   k_select_best: argmin over the B polished seeds (Alg. 2 l.9-10, R27) with a
-//     warp-shuffle + shared-memory reduction of the same 64-bit keys.
+//   k_select_best: argmin over the B polished seeds (Alg. 2 l.9-10, R27: fine-
+//     converged seeds first, then cost, then slot) with a warp-shuffle +
+//     shared-memory reduction of 64-bit keys (tier | cost bits | slot).
 //   k_fk: batched FK + Jacobian (Eqs. 1, 7), one thread per configuration.
 #include "kin.cuh"
 
@@ -79,7 +80,9 @@ k_select_best(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCf
     for (int b = threadIdx.x; b < used; b += blockDim.x) {
         const float pe = ep_all[(long long)t * B + b], oe = eo_all[(long long)t * B + b];
         const float cst = c.w_p * c.w_p * pe * pe + c.w_o * c.w_o * oe * oe;   // R14
-        const unsigned long long key = ((unsigned long long)cost_bits(cst) << 32) | (unsigned)b;
+        // R27: converged seeds first (bit 63), then cost, then slot
+        const unsigned long long tier = (pe < c.eps_p_fine && oe < c.eps_o_fine) ? 0ull : 1ull;
+        const unsigned long long key = (tier << 63) | ((unsigned long long)cost_bits(cst) << 32) | (unsigned)b;
         best = key < best ? key : best;
     }
 #pragma unroll

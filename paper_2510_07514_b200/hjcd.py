@@ -330,11 +330,12 @@ def pjik(robot: Robot, cfg: hjcd_config, targets, seeds, stream=None):
     _dev_f32(targets, (T, 7), "targets")
     _dev_f32(seeds, (T, cfg.B, n), "seeds")
     d = targets.device
-    out = dict(theta=torch.full((T, cfg.B, n), float("nan"), dtype=torch.float32, device=d),
-               ep=torch.full((T, cfg.B), float("nan"), dtype=torch.float32, device=d),
-               eo=torch.full((T, cfg.B), float("nan"), dtype=torch.float32, device=d),
-               counts=torch.zeros((T, cfg.B, 4), dtype=torch.int32, device=d),
-               iters=torch.zeros((T, cfg.B), dtype=torch.int32, device=d))
+    # slots >= floor(B/K)*K are not written by the kernel (left uninitialised)
+    out = dict(theta=torch.empty((T, cfg.B, n), dtype=torch.float32, device=d),
+               ep=torch.empty((T, cfg.B), dtype=torch.float32, device=d),
+               eo=torch.empty((T, cfg.B), dtype=torch.float32, device=d),
+               counts=torch.empty((T, cfg.B, 4), dtype=torch.int32, device=d),
+               iters=torch.empty((T, cfg.B), dtype=torch.int32, device=d))
     _check(lib().hjcd_pjik(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(seeds),
                            _ptr(out["theta"]), _ptr(out["ep"]), _ptr(out["eo"]),
                            _ptr(out["counts"]), _ptr(out["iters"]), _stream(stream)), "hjcd_pjik")
