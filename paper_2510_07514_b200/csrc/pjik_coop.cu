@@ -1,0 +1,295 @@
+// pjik_coop.cu — k_pjik_coop: PJ-IK (Alg. 4) for one target per CTA
+// with the per-target stop rule (Alg. 4 l.18 break; DESIGN.md
+// R26b) and WARP-COOPERATIVE line-search trials (K6).
+//
+// The B polish seeds of a target advance in lockstep (one thread per seed); the
+// CTA votes after each iteration's fine test and stops at the first iteration
+// in which any seed converged.  In lockstep, an iteration lasts as long as its
+// slowest seed: a seed whose LM step fails runs the whole fallback cascade
+// (A further LM trials, a dogleg trial, A+1 single-coordinate trials: up to
+// 2A+2 FKs) while the other 31 lanes of its warp idle.  Here every lane first
+// evaluates its own LM trial at alpha = 1 (the common case); seeds that fail
+// publish theta, their three directions, W, c0 and |rho|^2 to shared memory,
+// and ALL 32 lanes of the warp evaluate the pending trials of those seeds in
+// parallel.  Each failing seed then takes the FIRST successful trial in cascade
+// order (LM alpha_1..alpha_A, dogleg, single alpha_0..alpha_A) — exactly the
+// step the sequential cascade takes; extra evaluations have no side effects.
+#include "polish.cuh"
+
+namespace hjcd {
+
+// per-seed shared-memory record, structure-of-arrays with stride = blockDim.x
+struct CoopSmem {
+    float* th;     // [NMAX][nt]
+    float* dir;    // [3][NMAX][nt]   LM, dogleg, single-coordinate directions
+    float* W;      // [6][nt]
+    float* c0;     // [nt]
+    float* n0;     // [nt]
+    int* flags;    // [nt]  bit0 LM, bit1 dogleg, bit2 single
+    int* incl;     // [nt]  inclusive prefix of pending items within the warp
+    unsigned long long* ok;   // [nt]  success bits in cascade order
+};
+
+template <int NMAX>
+__device__ __forceinline__ CoopSmem coop_smem(void* base, int nt) {
+    CoopSmem s;
+    unsigned long long* p64 = (unsigned long long*)base;
+    s.ok = p64;
+    float* f = (float*)(p64 + nt);
+    s.th = f; f += NMAX * nt;
+    s.dir = f; f += 3 * NMAX * nt;
+    s.W = f; f += 6 * nt;
+    s.c0 = f; f += nt;
+    s.n0 = f; f += nt;
+    s.flags = (int*)f;
+    s.incl = s.flags + nt;
+    return s;
+}
+
+template <int NMAX>
+size_t coop_smem_bytes(int nt) {
+    return (size_t)nt * (8 + 4 * (4 * NMAX + 6 + 2) + 4 * 2);
+}
+
+// cascade item q of a seed with flags f -> (direction kind, alpha index)
+__device__ __forceinline__ void decode_item(int q, int f, int A, int& kind, int& a) {
+    const int nlm = (f & 1) ? A : 0;
+    const int ndl = (f & 2) ? 1 : 0;
+    if (q < nlm) { kind = 0; a = q + 1; return; }
+    q -= nlm;
+    if (q < ndl) { kind = 1; a = 0; return; }
+    kind = 2;
+    a = q - ndl;
+}
+
+template <int NMAX>
+__global__ void __launch_bounds__(256)
+k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
+            const float* __restrict__ targets, const float* __restrict__ seeds,
+            float* __restrict__ theta_out, float* __restrict__ ep_out, float* __restrict__ eo_out,
+            int32_t* __restrict__ counts_out, int32_t* __restrict__ iters_out) {
+    extern __shared__ unsigned long long coop_raw[];
+    const int nt = blockDim.x;
+    const CoopSmem S = coop_smem<NMAX>(coop_raw, nt);
+    const int n = rb.n;
+    const int used = c.copies * c.K;
+    const int t = blockIdx.x;
+    const int b = threadIdx.x;
+    const int lane = b & 31;
+    const int wbase = b - lane;
+    const bool active = b < used;
+    const Target tg = load_target(targets + 7ll * t);
+    const uint32_t tid = (uint32_t)(c.tid_offset + t);
+    const long long row = (long long)t * c.B + b;
+
+    float th[NMAX], tt[NMAX], dth[NMAX];
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) th[j] = (active && j < n) ? seeds[row * n + j] : 0.f;
+
+    int cnt[4] = {0, 0, 0, 0};
+    float3 Jp[NMAX], Jo[NMAX];
+    Resid r;
+    int k;
+    for (k = 0;; ++k) {
+        float3 pe;
+        Quat qe;
+        bool conv = false;
+        if (active) {
+            fk<NMAX, true>(rb, th, Jp, Jo, pe, qe);
+            r = residual(tg, pe, qe);
+            conv = r.ep < c.eps_p_fine && r.eo < c.eps_o_fine;   // Alg. 4 l.18 (R26)
+        }
+        if (__syncthreads_or(conv)) break;                      // R26b: target stops
+        if (k == c.lm_iters) break;
+
+        bool need = false;
+        int flags = 0, items = 0;
+        if (active) {
+            // ---- Eq. 7 Jacobian, W (R17), D (R20), c_W(theta), |rho|^2
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j) {
+                if (j < n) {
+                    const float3 z = Jo[j];
+                    if (rb.j[j].type == HJCD_REVOLUTE) {
+                        Jp[j] = cross3(z, pe - Jp[j]);
+                    } else {
+                        Jp[j] = z;
+                        Jo[j] = f3(0.f, 0.f, 0.f);
+                    }
+                }
+            }
+            float W[6], invD[NMAX];
+            {
+                float rn[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int j = 0; j < NMAX; ++j) {
+                    if (j < n) {
+                        rn[0] += Jp[j].x * Jp[j].x; rn[1] += Jp[j].y * Jp[j].y; rn[2] += Jp[j].z * Jp[j].z;
+                        rn[3] += Jo[j].x * Jo[j].x; rn[4] += Jo[j].y * Jo[j].y; rn[5] += Jo[j].z * Jo[j].z;
+                        invD[j] = 1.f / fmaxf(dot3(Jp[j], Jp[j]) + dot3(Jo[j], Jo[j]), c.d_floor);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 6; ++i) W[i] = (i < 3 ? c.w_p : c.w_o) / (1.f + sqrtf(rn[i]));
+            }
+            const float c0 = cost_w(W, r.rho);
+            // ---- own LM trial at alpha = 1 (Alg. 4 l.3-9, first element of A)
+            bool accepted = false;
+            const bool have_lm = lm_direction<NMAX>(rb, c, Jp, Jo, invD, W, r.rho, dth);
+            if (have_lm) {
+#pragma unroll
+                for (int j = 0; j < NMAX; ++j)
+                    if (j < n) tt[j] = clampf(th[j] + dth[j], rb.j[j].lo, rb.j[j].hi);
+                const Resid rt = eval_at<NMAX>(rb, tg, tt);
+                if (cost_w(W, rt.rho) < c0) {
+                    accepted = true;
+                    cnt[0]++;
+#pragma unroll
+                    for (int j = 0; j < NMAX; ++j) th[j] = tt[j];
+                }
+            }
+            if (!accepted) {
+                // publish the rest of the cascade for the warp
+                float n0 = 0.f;
+#pragma unroll
+                for (int i = 0; i < 6; ++i) n0 += r.rho[i] * r.rho[i];
+                flags = have_lm ? 1 : 0;
+#pragma unroll
+                for (int j = 0; j < NMAX; ++j) {
+                    S.th[j * nt + b] = th[j];
+                    S.dir[(0 * NMAX + j) * nt + b] = dth[j];
+                }
+                if (dogleg_direction<NMAX>(rb, c, Jp, Jo, r.rho, dth, tt)) {
+                    flags |= 2;
+#pragma unroll
+                    for (int j = 0; j < NMAX; ++j) S.dir[(1 * NMAX + j) * nt + b] = dth[j];
+                }
+                if (single_coord_direction<NMAX>(rb, c, Jp, Jo, W, r.rho, dth)) {
+                    flags |= 4;
+#pragma unroll
+                    for (int j = 0; j < NMAX; ++j) S.dir[(2 * NMAX + j) * nt + b] = dth[j];
+                }
+#pragma unroll
+                for (int i = 0; i < 6; ++i) S.W[i * nt + b] = W[i];
+                S.c0[b] = c0;
+                S.n0[b] = n0;
+                S.flags[b] = flags;
+                items = ((flags & 1) ? c.A : 0) + ((flags & 2) ? 1 : 0) + ((flags & 4) ? c.A + 1 : 0);
+                need = true;
+            }
+        }
+
+        // ---- warp-cooperative evaluation of the pending cascade trials (K6)
+        const unsigned needmask = __ballot_sync(0xffffffffu, need);
+        if (needmask) {
+            int incl = items;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl += v;
+            }
+            S.incl[b] = incl;
+            S.ok[b] = 0ull;
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            __syncwarp();
+            for (int it = lane; it < total; it += 32) {
+                // owner = first lane whose inclusive prefix exceeds it
+                int lo = 0, hi = 31;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (S.incl[wbase + mid] > it) hi = mid; else lo = mid + 1;
+                }
+                const int o = wbase + lo;
+                const int qq = it - (lo > 0 ? S.incl[o - 1] : 0);   // item index within the owner's list
+                int kind, a;
+                decode_item(qq, S.flags[o], c.A, kind, a);
+                float alpha = 1.f;
+                for (int i = 0; i < a; ++i) alpha *= c.inv_beta;
+                float x[NMAX];
+#pragma unroll
+                for (int j = 0; j < NMAX; ++j)
+                    x[j] = (j < n) ? clampf(S.th[j * nt + o] + alpha * S.dir[(kind * NMAX + j) * nt + o],
+                                            rb.j[j].lo, rb.j[j].hi)
+                                   : 0.f;
+                const Resid rt = eval_at<NMAX>(rb, tg, x);
+                bool ok;
+                if (kind == 1) {   // dogleg: unweighted |rho| (R23)
+                    float nt2 = 0.f;
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) nt2 += rt.rho[i] * rt.rho[i];
+                    ok = nt2 < S.n0[o];
+                } else {           // Eq. 13 with W frozen at theta (R22)
+                    float s = 0.f;
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) {
+                        const float wr = S.W[i * nt + o] * rt.rho[i];
+                        s += wr * wr;
+                    }
+                    ok = 0.5f * s < S.c0[o];
+                }
+                if (ok) atomicOr(&S.ok[o], 1ull << qq);
+            }
+            __syncwarp();
+            if (need) {
+                const unsigned long long m = S.ok[b];
+                if (m) {
+                    const int qq = __ffsll((long long)m) - 1;   // first success in cascade order
+                    int kind, a;
+                    decode_item(qq, flags, c.A, kind, a);
+                    float alpha = 1.f;
+                    for (int i = 0; i < a; ++i) alpha *= c.inv_beta;
+#pragma unroll
+                    for (int j = 0; j < NMAX; ++j)
+                        if (j < n)
+                            th[j] = clampf(th[j] + alpha * S.dir[(kind * NMAX + j) * nt + b], rb.j[j].lo, rb.j[j].hi);
+                    cnt[kind]++;
+                } else {
+                    perturb<NMAX>(rb, c, th, c.sigma_lm, tid, (uint32_t)b, P_PJPERT, (uint32_t)k);   // R25
+                    cnt[3]++;
+                }
+            }
+            __syncwarp();
+        }
+    }
+
+    if (!active) return;
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j)
+        if (j < n) theta_out[row * n + j] = th[j];
+    ep_out[row] = r.ep;
+    eo_out[row] = r.eo;
+    if (counts_out) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) counts_out[row * 4 + i] = cnt[i];
+    }
+    if (iters_out) iters_out[row] = k;
+}
+
+template <int NMAX>
+static cudaError_t launch_coop_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+                                 const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
+                                 int32_t* iters, cudaStream_t s) {
+    const int used = c.copies * c.K;
+    const int block = (used + 31) / 32 * 32;
+    const size_t smem = coop_smem_bytes<NMAX>(block);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_pjik_coop<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)coop_smem_bytes<NMAX>(256));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_pjik_coop<NMAX><<<T, block, smem, s>>>(rb, c, targets, seeds, theta, ep, eo, counts, iters);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pjik_coop(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+                             const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
+                             int32_t* iters, cudaStream_t s) {
+    if (c.copies * c.K > 256 || 2 * c.A + 2 > 64) return cudaErrorInvalidConfiguration;
+    if (rb.n <= 8) return launch_coop_t<8>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+    if (rb.n <= 16) return launch_coop_t<16>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+    return launch_coop_t<32>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+}
+
+}  // namespace hjcd

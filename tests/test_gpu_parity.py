@@ -197,6 +197,25 @@ def test_pjik_target_early_exit_parity(hjcd_lib, cuda, name, sigma):
     assert not (clean[same] & ~agree[same]).any()
 
 
+@pytest.mark.parametrize("name", ["panda", "fetch"])
+def test_pjik_cooperative_cascade_is_exact(hjcd_lib, cuda, name):
+    # K6: the warp-cooperative cascade (target_early_exit = 1) must give exactly
+    # the sequential per-seed cascade truncated at the target's k* (bitwise)
+    ch = inputs.robot(name)
+    rb = hjcd_lib.Robot(ch)
+    Tn, B = 12, 100
+    tg, th0 = targets_for(ch, Tn, start=40)
+    seeds = inputs.near_configs(ch, np.repeat(th0[:, None, :], B, 1), 0.3, seed=4).astype(np.float32)
+    p = params(B=B, K=50, lm_iters=64, target_early_exit=1)
+    ex = hjcd_lib.pjik(rb, hjcd_lib.config_from_params(p), T(tg, cuda), T(seeds, cuda))
+    kst = N(ex["iters"])[:, 0]
+    for t in range(Tn):
+        q = dict(p, target_early_exit=0, lm_iters=int(kst[t]), target_index_offset=t)
+        seq = hjcd_lib.pjik(rb, hjcd_lib.config_from_params(q), T(tg[t:t + 1], cuda), T(seeds[t:t + 1], cuda))
+        assert np.array_equal(N(seq["theta"])[0], N(ex["theta"])[t]), t
+        assert np.array_equal(N(seq["counts"])[0], N(ex["counts"])[t]), t
+
+
 def test_pjik_zero_error_fixed_point(hjcd_lib, cuda):
     ch = inputs.panda()
     rb = hjcd_lib.Robot(ch)
