@@ -286,6 +286,12 @@ def main():
         torch.cuda.synchronize()
         return r, e0.elapsed_time(e1)
 
+    # untimed pass first: the stage entry points allocate their outputs, and the
+    # caching allocator's first cudaMalloc must not land inside an event pair
+    o1 = hjcd.poccd(robot, cfg, targets)
+    seeds, _ = hjcd.select_replicate(robot, cfg, o1["cost"], o1["theta"])
+    o2 = hjcd.pjik(robot, cfg, targets, seeds)
+    hjcd.select_best(robot, cfg, targets, o2["theta"], o2["ep"], o2["eo"])
     for s in range(nb):
         o1, t1 = timed(lambda: hjcd.poccd(robot, cfg, targets))
         (seeds, _), t2 = timed(lambda: hjcd.select_replicate(robot, cfg, o1["cost"], o1["theta"]))
