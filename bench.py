@@ -164,7 +164,8 @@ def oracle_params(M, K, B):
                 eps_p_fine=1e-6, eps_o_fine=1e-5, gamma=1e-6, delta0=1.0, delta_rho=0.98,
                 delta_min=0.1, sigma_ccd=0.05, sigma_rep=0.02, sigma_lm=0.05, d_floor=1e-8, R=0.5,
                 beta=2.0, A=8, w_p=1.0, w_o=0.5, succ_p=1e-3, succ_o=math.pi / 180, tau_deg=1e-5,
-                rng_seed=0, repl_noise_all=0, target_early_exit=1, **{"lambda": 1e-3})
+                rng_seed=0, repl_noise_all=0, target_early_exit=1, ccd_early_exit=1,
+                **{"lambda": 1e-3})
 
 
 def cpu_baseline(cfgname, budget_s=12.0):

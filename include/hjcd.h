@@ -69,7 +69,8 @@ typedef enum { HJCD_REVOLUTE = 0, HJCD_PRISMATIC = 1, HJCD_FIXED = 2 } hjcd_join
  * The joint's frame is parent * origin; it then rotates about (revolute) or
  * translates along (prismatic) `axis`, expressed in that frame.
  * origin_quat_wxyz must be unit (+-1e-6); axis non-zero (normalised here);
- * lo <= hi (radians, or metres for prismatic).  Fixed joints are folded. */
+ * lo <= hi (radians, or metres for prismatic); revolute limits within +-1e4 rad
+ * (the kernels' joint sincos range).  Fixed joints are folded. */
 typedef struct {
     int32_t type;
     double origin_xyz[3];
@@ -107,6 +108,10 @@ typedef struct {
                                       first iteration in which ANY of its polish seeds passes the fine
                                       test (deterministic, needs floor(B/K)*K <= 256); 0 = every seed
                                       runs until it converges or lm_iters (per-seed freeze) */
+    int32_t ccd_early_exit;        /* PO-CCD stop rule (R12b): 1 = a target's M seeds stop at the
+                                      first iteration in which ANY of them passes the coarse test (one
+                                      thread-block cluster per target, deterministic, needs M <= 2048);
+                                      0 = every seed runs until it converges or ccd_iters */
     float eps_p_coarse, eps_o_coarse; /* epsilon [m], nu [rad], Alg. 3 l.14 (R12) */
     float eps_p_fine, eps_o_fine;  /* varepsilon [m], upsilon [rad], Alg. 4 l.18 (R26) */
     float gamma;                   /* improvement threshold, Alg. 3 l.11 (R10) */

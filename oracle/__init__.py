@@ -53,7 +53,8 @@ class OracleConfig(C.Structure):
                 ("R", C.c_double), ("beta", C.c_double), ("A", C.c_int32),
                 ("w_p", C.c_double), ("w_o", C.c_double), ("succ_p", C.c_double),
                 ("succ_o", C.c_double), ("tau_deg", C.c_double), ("rng_seed", C.c_uint64),
-                ("repl_noise_all", C.c_int32), ("target_early_exit", C.c_int32)]
+                ("repl_noise_all", C.c_int32), ("target_early_exit", C.c_int32),
+                ("ccd_early_exit", C.c_int32)]
 
 
 _lib = None

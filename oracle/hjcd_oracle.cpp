@@ -80,6 +80,7 @@ typedef struct {
     uint64_t rng_seed;
     int32_t repl_noise_all;
     int32_t target_early_exit;
+    int32_t ccd_early_exit;
 } OracleConfig;
 
 } /* extern "C" */
@@ -429,112 +430,157 @@ double ccd_orientation_step(double phi, V3 a, V3 rj, double dk) {
 /* ---------------- PO-CCD one seed (Alg. 3) ---------------- */
 struct SeedOut { double ep, eo; int iters; double margin; };
 
-SeedOut po_ccd_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
-                    uint32_t sid, std::vector<double>& th) {
-    const OracleRobot* r = rb.r;
-    int n = rb.dof;
-    SeedOut so;
-    so.margin = INF;
-    Frames F, Fc;
-    std::vector<double> thc(n), thh(n);
-    int k = 0;
-    Err e;
-    for (k = 0;; ++k) {
-        fk(rb, th.data(), F);
-        e = residual(F, tgt);
-        /* Alg. 3 l.14, unsquared reading R12; checked at iteration
-         * start so a seed on the answer stops with 0 updates */
-        bool cp = e.ep < c.eps_p_coarse, co = e.eo < c.eps_o_coarse;
-        so.margin = std::min(so.margin, margin_and(cp, std::fabs(e.ep - c.eps_p_coarse), co,
-                                                   std::fabs(e.eo - c.eps_o_coarse)));
-        if (cp && co) break;
-        if (k == c.ccd_iters) break;
-
-        double phi; V3 ahat;
-        angle_axis(tgt.q, F.qee, &phi, &ahat);
-        double dk = delta_k(c, k);
-        /* the w >= 0 canonicalisation of q_err flips a (R1/R2) when w crosses 0 */
-        if (phi > 0) so.margin = std::min(so.margin, std::fabs(std::cos(phi / 2.0)));
-        std::vector<double> sp(n), sop(n), dp(n), dor(n);
-        for (int j = 0; j < n; ++j) {
-            int ent = rb.dof_entry[j];
-            double lo = r->lo[ent], hi = r->hi[ent];
-            /* position candidate (Eqs. 8-9); prismatic: z.(P_t - P_ee) (R32) */
-            double stepp;
-            if (r->type[ent] == 0) {
-                double mdeg;
-                stepp = ccd_position_step(F.P[j], F.z[j], F.pee, tgt.p, c.tau_deg, &mdeg);
-                so.margin = std::min(so.margin, mdeg);
-            } else {
-                stepp = dot(F.z[j], sub(tgt.p, F.pee));
-            }
-            /* joint limits on candidates (R7) */
-            dp[j] = clampd(th[j] + stepp, lo, hi) - th[j];
-            thc = th; thc[j] = th[j] + dp[j];
-            fk(rb, thc.data(), Fc);                     /* literal P:222: full FK */
-            sp[j] = norm(sub(tgt.p, Fc.pee));
-            /* orientation candidate (Eqs. 10-11); prismatic: 0 */
-            double stepo = 0.0;
-            if (r->type[ent] == 0) {
-                stepo = ccd_orientation_step(phi, ahat, F.z[j], dk);
-                if (phi > 0) so.margin = std::min(so.margin, std::fabs(dot(ahat, F.z[j])));
-            }
-            dor[j] = clampd(th[j] + stepo, lo, hi) - th[j];
-            thc = th; thc[j] = th[j] + dor[j];
-            fk(rb, thc.data(), Fc);
-            sop[j] = norm(quat_error(tgt.q, Fc.qee));
-        }
-        /* Alg. 3 l.9: argmin over joints, ties -> lower index (R6) */
-        int jp = 0, jo = 0;
-        for (int j = 1; j < n; ++j) {
-            if (sp[j] < sp[jp]) jp = j;
-            if (sop[j] < sop[jo]) jo = j;
-        }
-        for (int j = 0; j < n; ++j) {
-            /* distance to the nearest competitor with a different outcome */
-            if (j != jp && (dp[j] != 0.0 || dp[jp] != 0.0))
-                so.margin = std::min(so.margin, std::fabs(sp[j] - sp[jp]));
-            if (j != jo && (dor[j] != 0.0 || dor[jo] != 0.0))
-                so.margin = std::min(so.margin, std::fabs(sop[j] - sop[jo]));
-        }
-        /* Alg. 3 l.10 + P:201: same joint -> larger |dtheta|, tie -> position (R8) */
-        thh = th;
-        if (jp == jo) {
-            if (dp[jp] != dor[jo]) /* equal steps = same outcome, no decision */
-                so.margin = std::min(so.margin, std::fabs(std::fabs(dp[jp]) - std::fabs(dor[jo])));
-            if (std::fabs(dp[jp]) >= std::fabs(dor[jo])) thh[jp] = th[jp] + dp[jp];
-            else thh[jo] = th[jo] + dor[jo];
-        } else {
-            thh[jp] = th[jp] + dp[jp];
-            thh[jo] = th[jo] + dor[jo];
-        }
-        /* clamp after every applied update (R7): removes rounding overshoot */
-        for (int j = 0; j < n; ++j) {
-            int ent = rb.dof_entry[j];
-            thh[j] = clampd(thh[j], r->lo[ent], r->hi[ent]);
-        }
-        fk(rb, thh.data(), Fc);
-        Err eh = residual(Fc, tgt);
-        /* Alg. 3 l.11 read as an improvement test on either space (R10) */
-        double ip = e.ep - eh.ep, io = e.eo - eh.eo;
-        bool ap = ip > c.gamma, ao = io > c.gamma;
-        so.margin = std::min(so.margin, margin_or(ap, std::fabs(ip - c.gamma), ao,
-                                                  std::fabs(io - c.gamma)));
-        if (ap || ao) {
-            th = thh;
-        } else {
-            /* Alg. 3 l.13: theta + N(0, sigma_ccd^2 I), clamp (R11) */
-            for (int j = 0; j < n; ++j) {
-                int ent = rb.dof_entry[j];
-                double g = normal_for_joint(c.rng_seed, tid, sid, P_PERTURB, (uint32_t)k, j);
-                th[j] = clampd(th[j] + c.sigma_ccd * g, r->lo[ent], r->hi[ent]);
-            }
-        }
-    }
+/* Alg. 3 l.14, unsquared reading R12, checked at iteration start so a
+ * seed on the answer stops with 0 updates: FK, residual, coarse test. */
+bool po_ccd_check(const Robot& rb, const OracleConfig& c, const Target& tgt,
+                  const std::vector<double>& th, Frames& F, Err& e, SeedOut& so) {
+    fk(rb, th.data(), F);
+    e = residual(F, tgt);
+    bool cp = e.ep < c.eps_p_coarse, co = e.eo < c.eps_o_coarse;
+    so.margin = std::min(so.margin, margin_and(cp, std::fabs(e.ep - c.eps_p_coarse), co,
+                                               std::fabs(e.eo - c.eps_o_coarse)));
     so.ep = e.ep;
     so.eo = e.eo;
+    return cp && co;
+}
+
+/* Alg. 3 l.6-13: one greedy orientation-aware update of seed `sid`
+ * at iteration k (frames F and residual e at th), or a perturbation. */
+void po_ccd_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
+                 uint32_t sid, int k, const Frames& F, const Err& e, std::vector<double>& th,
+                 SeedOut& so) {
+    const OracleRobot* r = rb.r;
+    int n = rb.dof;
+    Frames Fc;
+    std::vector<double> thc(n), thh(n);
+    double phi; V3 ahat;
+    angle_axis(tgt.q, F.qee, &phi, &ahat);
+    double dk = delta_k(c, k);
+    /* the w >= 0 canonicalisation of q_err flips a (R1/R2) when w crosses 0 */
+    if (phi > 0) so.margin = std::min(so.margin, std::fabs(std::cos(phi / 2.0)));
+    std::vector<double> sp(n), sop(n), dp(n), dor(n);
+    for (int j = 0; j < n; ++j) {
+        int ent = rb.dof_entry[j];
+        double lo = r->lo[ent], hi = r->hi[ent];
+        /* position candidate (Eqs. 8-9); prismatic: z.(P_t - P_ee) (R32) */
+        double stepp;
+        if (r->type[ent] == 0) {
+            double mdeg;
+            stepp = ccd_position_step(F.P[j], F.z[j], F.pee, tgt.p, c.tau_deg, &mdeg);
+            so.margin = std::min(so.margin, mdeg);
+        } else {
+            stepp = dot(F.z[j], sub(tgt.p, F.pee));
+        }
+        /* joint limits on candidates (R7) */
+        dp[j] = clampd(th[j] + stepp, lo, hi) - th[j];
+        thc = th; thc[j] = th[j] + dp[j];
+        fk(rb, thc.data(), Fc);                     /* literal P:222: full FK */
+        sp[j] = norm(sub(tgt.p, Fc.pee));
+        /* orientation candidate (Eqs. 10-11); prismatic: 0 */
+        double stepo = 0.0;
+        if (r->type[ent] == 0) {
+            stepo = ccd_orientation_step(phi, ahat, F.z[j], dk);
+            if (phi > 0) so.margin = std::min(so.margin, std::fabs(dot(ahat, F.z[j])));
+        }
+        dor[j] = clampd(th[j] + stepo, lo, hi) - th[j];
+        thc = th; thc[j] = th[j] + dor[j];
+        fk(rb, thc.data(), Fc);
+        sop[j] = norm(quat_error(tgt.q, Fc.qee));
+    }
+    /* Alg. 3 l.9: argmin over joints, ties -> lower index (R6) */
+    int jp = 0, jo = 0;
+    for (int j = 1; j < n; ++j) {
+        if (sp[j] < sp[jp]) jp = j;
+        if (sop[j] < sop[jo]) jo = j;
+    }
+    for (int j = 0; j < n; ++j) {
+        /* distance to the nearest competitor with a different outcome */
+        if (j != jp && (dp[j] != 0.0 || dp[jp] != 0.0))
+            so.margin = std::min(so.margin, std::fabs(sp[j] - sp[jp]));
+        if (j != jo && (dor[j] != 0.0 || dor[jo] != 0.0))
+            so.margin = std::min(so.margin, std::fabs(sop[j] - sop[jo]));
+    }
+    /* Alg. 3 l.10 + P:201: same joint -> larger |dtheta|, tie -> position (R8) */
+    thh = th;
+    if (jp == jo) {
+        if (dp[jp] != dor[jo]) /* equal steps = same outcome, no decision */
+            so.margin = std::min(so.margin, std::fabs(std::fabs(dp[jp]) - std::fabs(dor[jo])));
+        if (std::fabs(dp[jp]) >= std::fabs(dor[jo])) thh[jp] = th[jp] + dp[jp];
+        else thh[jo] = th[jo] + dor[jo];
+    } else {
+        thh[jp] = th[jp] + dp[jp];
+        thh[jo] = th[jo] + dor[jo];
+    }
+    /* clamp after every applied update (R7): removes rounding overshoot */
+    for (int j = 0; j < n; ++j) {
+        int ent = rb.dof_entry[j];
+        thh[j] = clampd(thh[j], r->lo[ent], r->hi[ent]);
+    }
+    fk(rb, thh.data(), Fc);
+    Err eh = residual(Fc, tgt);
+    /* Alg. 3 l.11 read as an improvement test on either space (R10) */
+    double ip = e.ep - eh.ep, io = e.eo - eh.eo;
+    bool ap = ip > c.gamma, ao = io > c.gamma;
+    so.margin = std::min(so.margin, margin_or(ap, std::fabs(ip - c.gamma), ao,
+                                              std::fabs(io - c.gamma)));
+    if (ap || ao) {
+        th = thh;
+    } else {
+        /* Alg. 3 l.13: theta + N(0, sigma_ccd^2 I), clamp (R11) */
+        for (int j = 0; j < n; ++j) {
+            int ent = rb.dof_entry[j];
+            double g = normal_for_joint(c.rng_seed, tid, sid, P_PERTURB, (uint32_t)k, j);
+            th[j] = clampd(th[j] + c.sigma_ccd * g, r->lo[ent], r->hi[ent]);
+        }
+    }
+}
+
+SeedOut seed_init() {
+    SeedOut so;
+    so.ep = so.eo = INF;
+    so.iters = 0;
+    so.margin = INF;
+    return so;
+}
+
+/* Alg. 3 for ONE seed with a per-seed break (ccd_early_exit = 0) */
+SeedOut po_ccd_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
+                    uint32_t sid, std::vector<double>& th) {
+    SeedOut so = seed_init();
+    Frames F;
+    Err e;
+    int k;
+    for (k = 0;; ++k) {
+        if (po_ccd_check(rb, c, tgt, th, F, e, so)) break;
+        if (k == c.ccd_iters) break;
+        po_ccd_step(rb, c, tgt, tid, sid, k, F, e, th, so);
+    }
     so.iters = k;
     return so;
+}
+
+/* Alg. 3 for the M seeds of ONE target with the paper's stop rule ("once
+ * a seed satisfies the position and orientation error thresholds ... the
+ * parallel loop is broken and all samples are returned"; ccd_early_exit = 1,
+ * DESIGN.md R12b).  The M seeds advance in lockstep (iteration loop outside,
+ * seeds inside); the target stops at the first iteration at which any seed
+ * passes the coarse test, every seed keeping its state after that many
+ * iterations.  th_m: [M][n] in/out. */
+void po_ccd_target(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid, int M,
+                   std::vector<std::vector<double>>& th_m, std::vector<SeedOut>& so) {
+    so.assign(M, seed_init());
+    std::vector<Frames> F(M);
+    std::vector<Err> e(M);
+    for (int k = 0;; ++k) {
+        bool any = false;
+        for (int m = 0; m < M; ++m) {
+            bool cv = po_ccd_check(rb, c, tgt, th_m[m], F[m], e[m], so[m]);
+            any = any || cv;
+        }
+        for (int m = 0; m < M; ++m) so[m].iters = k;
+        if (any || k == c.ccd_iters) break;
+        for (int m = 0; m < M; ++m) po_ccd_step(rb, c, tgt, tid, (uint32_t)m, k, F[m], e[m], th_m[m], so[m]);
+    }
 }
 
 /* uniform seed in limits (Alg. 3 l.2-3), fp32 fmaf on purpose (R30) */
@@ -1013,22 +1059,41 @@ void oracle_po_ccd(const OracleRobot* r, const OracleConfig* c, const float* tar
                    double* ep, double* eo, int32_t* iters, double* margin) {
     Robot rb = make_robot(r);
     int n = rb.dof, M = c->M;
+    auto seed_of = [&](int t, int m, uint64_t tid, std::vector<double>& th) {
+        if (seeds) for (int j = 0; j < n; ++j) th[j] = seeds[((size_t)t * n + j) * M + m];
+        else uniform_seed(rb, c->rng_seed, tid, (uint32_t)m, th.data());
+    };
+    auto emit = [&](int t, int m, const std::vector<double>& th, const SeedOut& so) {
+        for (int j = 0; j < n; ++j) theta[((size_t)t * n + j) * M + m] = th[j];
+        size_t o = (size_t)t * M + m;
+        if (cost) cost[o] = rank_cost(*c, so.ep, so.eo);
+        if (ep) ep[o] = so.ep;
+        if (eo) eo[o] = so.eo;
+        if (iters) iters[o] = so.iters;
+        if (margin) margin[o] = so.margin;
+    };
+    if (c->ccd_early_exit) {
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int t = 0; t < T; ++t) {
+            Target tgt = read_target(targets + (size_t)t * 7);
+            uint64_t tid = (uint64_t)(tid_offset + t);
+            std::vector<std::vector<double>> th(M, std::vector<double>(n));
+            for (int m = 0; m < M; ++m) seed_of(t, m, tid, th[m]);
+            std::vector<SeedOut> so;
+            po_ccd_target(rb, *c, tgt, tid, M, th, so);
+            for (int m = 0; m < M; ++m) emit(t, m, th[m], so[m]);
+        }
+        return;
+    }
 #pragma omp parallel for collapse(2) schedule(dynamic, 4)
     for (int t = 0; t < T; ++t) {
         for (int m = 0; m < M; ++m) {
             Target tgt = read_target(targets + (size_t)t * 7);
             uint64_t tid = (uint64_t)(tid_offset + t);
             std::vector<double> th(n);
-            if (seeds) for (int j = 0; j < n; ++j) th[j] = seeds[((size_t)t * n + j) * M + m];
-            else uniform_seed(rb, c->rng_seed, tid, (uint32_t)m, th.data());
+            seed_of(t, m, tid, th);
             SeedOut so = po_ccd_seed(rb, *c, tgt, tid, (uint32_t)m, th);
-            for (int j = 0; j < n; ++j) theta[((size_t)t * n + j) * M + m] = th[j];
-            size_t o = (size_t)t * M + m;
-            if (cost) cost[o] = rank_cost(*c, so.ep, so.eo);
-            if (ep) ep[o] = so.ep;
-            if (eo) eo[o] = so.eo;
-            if (iters) iters[o] = so.iters;
-            if (margin) margin[o] = so.margin;
+            emit(t, m, th, so);
         }
     }
 }
@@ -1111,12 +1176,17 @@ void oracle_solve(const OracleRobot* r, const OracleConfig* c, const float* targ
         }
         /* stage 1: PO-CCD over M seeds */
         std::vector<double> theta_nm((size_t)n * M), cost(M);
-        std::vector<double> th(n);
+        std::vector<std::vector<double>> th1(M, std::vector<double>(n));
+        std::vector<SeedOut> so1(M);
+        for (int m = 0; m < M; ++m) uniform_seed(rb, c->rng_seed, tid, (uint32_t)m, th1[m].data());
+        if (c->ccd_early_exit) {
+            po_ccd_target(rb, *c, tgt, tid, M, th1, so1);   /* P:203 stop rule (R12b) */
+        } else {
+            for (int m = 0; m < M; ++m) so1[m] = po_ccd_seed(rb, *c, tgt, tid, (uint32_t)m, th1[m]);
+        }
         for (int m = 0; m < M; ++m) {
-            uniform_seed(rb, c->rng_seed, tid, (uint32_t)m, th.data());
-            SeedOut so = po_ccd_seed(rb, *c, tgt, tid, (uint32_t)m, th);
-            for (int j = 0; j < n; ++j) theta_nm[(size_t)j * M + m] = th[j];
-            cost[m] = rank_cost(*c, so.ep, so.eo);
+            for (int j = 0; j < n; ++j) theta_nm[(size_t)j * M + m] = th1[m][j];
+            cost[m] = rank_cost(*c, so1[m].ep, so1[m].eo);
         }
         /* top-K + replicate */
         std::vector<double> seeds((size_t)B * n);

@@ -115,6 +115,8 @@ hjcd_status build_robot(const hjcd_joint* joints, int32_t num, const double ee_x
             double na = std::sqrt(j.axis[0] * j.axis[0] + j.axis[1] * j.axis[1] + j.axis[2] * j.axis[2]);
             if (!(na > 1e-9)) return HJCD_E_INVALID_ARG;
             if (!std::isfinite(j.lo) || !std::isfinite(j.hi) || j.lo > j.hi) return HJCD_E_INVALID_ARG;
+            // the kernels' joint sincos is accurate for |theta| <= 1e4 (kin.cuh sincos_b)
+            if (j.type == HJCD_REVOLUTE && (std::fabs(j.lo) > 1e4 || std::fabs(j.hi) > 1e4)) return HJCD_E_INVALID_ARG;
             dof++;
         }
     }
@@ -166,6 +168,7 @@ hjcd_status make_cfg(const hjcd_robot* r, const hjcd_config* c, DevCfg* d) {
     if (c->ccd_iters < 0 || c->lm_iters < 0 || c->A < 0) return HJCD_E_INVALID_ARG;
     if (c->target_early_exit != 0 && c->target_early_exit != 1) return HJCD_E_INVALID_ARG;
     if (c->target_early_exit && ((c->B / c->K) * c->K > 256 || c->A > 31)) return HJCD_E_UNSUPPORTED;
+    if (c->ccd_early_exit != 0 && c->ccd_early_exit != 1) return HJCD_E_INVALID_ARG;
     if (!(c->beta > 1.f) || !(c->lambda > 0.f) || !(c->d_floor > 0.f) || !(c->R > 0.f)) return HJCD_E_INVALID_ARG;
     if (!(c->eps_p_coarse > 0.f) || !(c->eps_o_coarse > 0.f) || !(c->eps_p_fine > 0.f) ||
         !(c->eps_o_fine > 0.f))
@@ -178,6 +181,7 @@ hjcd_status make_cfg(const hjcd_robot* r, const hjcd_config* c, DevCfg* d) {
     d->copies = c->B / c->K;
     d->repl_noise_all = c->repl_noise_all ? 1 : 0;
     d->target_early_exit = c->target_early_exit;
+    d->ccd_early_exit = c->ccd_early_exit;
     d->eps_p_coarse = c->eps_p_coarse; d->eps_o_coarse = c->eps_o_coarse;
     d->eps_p_fine = c->eps_p_fine; d->eps_o_fine = c->eps_o_fine;
     d->gamma = c->gamma; d->delta0 = c->delta0; d->delta_rho = c->delta_rho; d->delta_min = c->delta_min;
@@ -189,6 +193,11 @@ hjcd_status make_cfg(const hjcd_robot* r, const hjcd_config* c, DevCfg* d) {
     d->key1 = (uint32_t)(c->rng_seed >> 32);
     d->tid_offset = c->target_index_offset;
     return HJCD_OK;
+}
+
+// the PO-CCD stop rule keeps a target's M seeds in one cluster of <= 16 x 128 threads
+hjcd_status check_poccd(const hjcd_config* c) {
+    return (c->ccd_early_exit && c->M > 2048) ? HJCD_E_UNSUPPORTED : HJCD_OK;
 }
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -250,6 +259,7 @@ void hjcd_config_default(hjcd_config* c) {
     c->M = 1000; c->K = 50; c->B = 100;            // R16
     c->ccd_iters = 64; c->lm_iters = 128;          // R28
     c->target_early_exit = 1;                           // R26b
+    c->ccd_early_exit = 1;                              // R12b
     c->eps_p_coarse = 5e-3f; c->eps_o_coarse = 5e-2f;   // R12
     c->eps_p_fine = 1e-6f; c->eps_o_fine = 1e-5f;       // R26
     c->gamma = 1e-6f;                                   // R10
@@ -269,6 +279,7 @@ hjcd_status hjcd_workspace_size(const hjcd_robot* r, int32_t T, const hjcd_confi
     DevCfg d;
     hjcd_status st = make_cfg(r, c, &d);
     if (st != HJCD_OK) return st;
+    if ((st = check_poccd(c)) != HJCD_OK) return st;
     *bytes = layout(r->dof, T, c).total;
     return HJCD_OK;
 }
@@ -289,6 +300,7 @@ hjcd_status hjcd_solve(const hjcd_robot* r, const hjcd_config* c, const float* t
     hjcd_status st = make_cfg(r, c, &d);
     if (st != HJCD_OK) return st;
     if (c->M > 8192) return HJCD_E_UNSUPPORTED;
+    if ((st = check_poccd(c)) != HJCD_OK) return st;
     Layout L = layout(r->dof, T, c);
     if (workspace_bytes < L.total || ((uintptr_t)workspace & 255)) return HJCD_E_WORKSPACE;
     char* ws = (char*)workspace;
@@ -361,6 +373,7 @@ hjcd_status hjcd_poccd(const hjcd_robot* r, const hjcd_config* c, const float* t
     DevCfg d;
     hjcd_status st = make_cfg(r, c, &d);
     if (st != HJCD_OK) return st;
+    if ((st = check_poccd(c)) != HJCD_OK) return st;
     cudaError_t e = launch_poccd(r->dev, d, targets, T, seeds, theta, cost, pos_err, ori_err, iters,
                                  (cudaStream_t)stream);
     return e == cudaSuccess ? HJCD_OK : cuda_fail(e);

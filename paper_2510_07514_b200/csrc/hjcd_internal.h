@@ -34,7 +34,7 @@ struct DevRobot {
 };
 
 struct DevCfg {
-    int32_t M, K, B, ccd_iters, lm_iters, A, copies, repl_noise_all, target_early_exit;
+    int32_t M, K, B, ccd_iters, lm_iters, A, copies, repl_noise_all, target_early_exit, ccd_early_exit;
     float eps_p_coarse, eps_o_coarse, eps_p_fine, eps_o_fine;
     float gamma, delta0, delta_rho, delta_min;
     float sigma_ccd, sigma_rep, sigma_lm;

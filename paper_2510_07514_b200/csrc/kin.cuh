@@ -100,13 +100,34 @@ __device__ __forceinline__ Quat quat_from_rot(const float R[9]) {
     return q;
 }
 
+// sin and cos of a joint angle (fp32, |err| <= 7.1e-8 on |x| <= 1e4; joint
+// angles are always clamped to their limits, which hjcd_robot_create bounds):
+// Cody-Waite reduction by pi/2 in two FMA steps, then the cephes sinf/cosf
+// minimax polynomials on [-pi/4, pi/4].  Branch-free and short: the library
+// sincosf carries a Payne-Hanek slow path (local memory, ~200 instructions)
+// per call site, which bloats the polish kernels' code (i-cache misses).
+__device__ __forceinline__ void sincos_b(float x, float* s, float* c) {
+    const float q = rintf(x * 0.636619772367581343f);
+    float r = fmaf(-q, 1.5707963705062866f, x);
+    r = fmaf(-q, -4.37113900018624283e-8f, r);
+    const float z = r * r;
+    const float ps = fmaf(fmaf(fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f), z, -1.6666654611e-1f), z * r, r);
+    const float pc = fmaf(fmaf(fmaf(fmaf(2.443315711809948e-5f, z, -1.388731625493765e-3f), z,
+                                    4.166664568298827e-2f), z, -0.5f), z, 1.0f);
+    const int qi = (int)q;
+    const float sa = (qi & 1) ? pc : ps;
+    const float ca = (qi & 1) ? ps : pc;
+    *s = (qi & 2) ? -sa : sa;
+    *c = ((qi + 1) & 2) ? -ca : ca;
+}
+
 // Forward kinematics (Eq. 1) with frames (Eq. 7 inputs):
 // T = F_1 Rz(th_1) F_2 Rz(th_2) ... F_n Rz(th_n) EE  (prismatic: Tz).
 // FRAMES: P[j] = joint origin, Z[j] = joint axis (world), before joint motion
 // (identical after it: rotation about z fixes the axis and the origin).
 // EXACT: the chain has exactly NMAX DoF (no per-joint guard).  FAST: joint
 // sincos on the SFU (__sincosf, |err| <~ 5e-7 rad on the joint ranges): used by
-// the coarse stage only (K5); the polish stage uses accurate sincosf.
+// the coarse stage only (K5); the polish stage uses sincos_b.
 template <int NMAX, bool FRAMES, bool EXACT = false, bool FAST = false>
 __device__ __forceinline__ void fk(const DevRobot& rb, const float (&th)[NMAX], float3 (&P)[NMAX],
                                    float3 (&Z)[NMAX], float3& pe, Quat& qe) {
@@ -132,7 +153,7 @@ __device__ __forceinline__ void fk(const DevRobot& rb, const float (&th)[NMAX], 
             if (J.type == HJCD_REVOLUTE) {
                 float s, c;
                 if (FAST) __sincosf(th[j], &s, &c);
-                else sincosf(th[j], &s, &c);
+                else sincos_b(th[j], &s, &c);
 #pragma unroll
                 for (int r = 0; r < 3; ++r) {
                     float a = N[3 * r], b = N[3 * r + 1];

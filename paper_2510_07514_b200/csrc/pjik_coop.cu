@@ -62,7 +62,7 @@ __device__ __forceinline__ void decode_item(int q, int f, int A, int& kind, int&
     a = q - ndl;
 }
 
-template <int NMAX>
+template <int NMAX, bool EXACT>
 __global__ void __launch_bounds__(256)
 k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
             const float* __restrict__ targets, const float* __restrict__ seeds,
@@ -84,7 +84,7 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
 
     float th[NMAX], tt[NMAX], dth[NMAX];
 #pragma unroll
-    for (int j = 0; j < NMAX; ++j) th[j] = (active && j < n) ? seeds[row * n + j] : 0.f;
+    for (int j = 0; j < NMAX; ++j) th[j] = (active && (EXACT || j < n)) ? seeds[row * n + j] : 0.f;
 
     int cnt[4] = {0, 0, 0, 0};
     float3 Jp[NMAX], Jo[NMAX];
@@ -95,7 +95,7 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
         Quat qe;
         bool conv = false;
         if (active) {
-            fk<NMAX, true>(rb, th, Jp, Jo, pe, qe);
+            fk<NMAX, true, EXACT>(rb, th, Jp, Jo, pe, qe);
             r = residual(tg, pe, qe);
             conv = r.ep < c.eps_p_fine && r.eo < c.eps_o_fine;   // Alg. 4 l.18 (R26)
         }
@@ -108,7 +108,7 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
             // ---- Eq. 7 Jacobian, W (R17), D (R20), c_W(theta), |rho|^2
 #pragma unroll
             for (int j = 0; j < NMAX; ++j) {
-                if (j < n) {
+                if (EXACT || j < n) {
                     const float3 z = Jo[j];
                     if (rb.j[j].type == HJCD_REVOLUTE) {
                         Jp[j] = cross3(z, pe - Jp[j]);
@@ -123,7 +123,7 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
                 float rn[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int j = 0; j < NMAX; ++j) {
-                    if (j < n) {
+                    if (EXACT || j < n) {
                         rn[0] += Jp[j].x * Jp[j].x; rn[1] += Jp[j].y * Jp[j].y; rn[2] += Jp[j].z * Jp[j].z;
                         rn[3] += Jo[j].x * Jo[j].x; rn[4] += Jo[j].y * Jo[j].y; rn[5] += Jo[j].z * Jo[j].z;
                         invD[j] = 1.f / fmaxf(dot3(Jp[j], Jp[j]) + dot3(Jo[j], Jo[j]), c.d_floor);
@@ -135,12 +135,12 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
             const float c0 = cost_w(W, r.rho);
             // ---- own LM trial at alpha = 1 (Alg. 4 l.3-9, first element of A)
             bool accepted = false;
-            const bool have_lm = lm_direction<NMAX>(rb, c, Jp, Jo, invD, W, r.rho, dth);
+            const bool have_lm = lm_direction<NMAX, EXACT>(rb, c, Jp, Jo, invD, W, r.rho, dth);
             if (have_lm) {
 #pragma unroll
                 for (int j = 0; j < NMAX; ++j)
-                    if (j < n) tt[j] = clampf(th[j] + dth[j], rb.j[j].lo, rb.j[j].hi);
-                const Resid rt = eval_at<NMAX>(rb, tg, tt);
+                    if (EXACT || j < n) tt[j] = clampf(th[j] + dth[j], rb.j[j].lo, rb.j[j].hi);
+                const Resid rt = eval_at<NMAX, EXACT>(rb, tg, tt);
                 if (cost_w(W, rt.rho) < c0) {
                     accepted = true;
                     cnt[0]++;
@@ -159,12 +159,12 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
                     S.th[j * nt + b] = th[j];
                     S.dir[(0 * NMAX + j) * nt + b] = dth[j];
                 }
-                if (dogleg_direction<NMAX>(rb, c, Jp, Jo, r.rho, dth, tt)) {
+                if (dogleg_direction<NMAX, EXACT>(rb, c, Jp, Jo, r.rho, dth, tt)) {
                     flags |= 2;
 #pragma unroll
                     for (int j = 0; j < NMAX; ++j) S.dir[(1 * NMAX + j) * nt + b] = dth[j];
                 }
-                if (single_coord_direction<NMAX>(rb, c, Jp, Jo, W, r.rho, dth)) {
+                if (single_coord_direction<NMAX, EXACT>(rb, c, Jp, Jo, W, r.rho, dth)) {
                     flags |= 4;
 #pragma unroll
                     for (int j = 0; j < NMAX; ++j) S.dir[(2 * NMAX + j) * nt + b] = dth[j];
@@ -208,10 +208,10 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
                 float x[NMAX];
 #pragma unroll
                 for (int j = 0; j < NMAX; ++j)
-                    x[j] = (j < n) ? clampf(S.th[j * nt + o] + alpha * S.dir[(kind * NMAX + j) * nt + o],
+                    x[j] = (EXACT || j < n) ? clampf(S.th[j * nt + o] + alpha * S.dir[(kind * NMAX + j) * nt + o],
                                             rb.j[j].lo, rb.j[j].hi)
                                    : 0.f;
-                const Resid rt = eval_at<NMAX>(rb, tg, x);
+                const Resid rt = eval_at<NMAX, EXACT>(rb, tg, x);
                 bool ok;
                 if (kind == 1) {   // dogleg: unweighted |rho| (R23)
                     float nt2 = 0.f;
@@ -240,11 +240,11 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
                     for (int i = 0; i < a; ++i) alpha *= c.inv_beta;
 #pragma unroll
                     for (int j = 0; j < NMAX; ++j)
-                        if (j < n)
+                        if (EXACT || j < n)
                             th[j] = clampf(th[j] + alpha * S.dir[(kind * NMAX + j) * nt + b], rb.j[j].lo, rb.j[j].hi);
                     cnt[kind]++;
                 } else {
-                    perturb<NMAX>(rb, c, th, c.sigma_lm, tid, (uint32_t)b, P_PJPERT, (uint32_t)k);   // R25
+                    perturb<NMAX, EXACT>(rb, c, th, c.sigma_lm, tid, (uint32_t)b, P_PJPERT, (uint32_t)k);   // R25
                     cnt[3]++;
                 }
             }
@@ -255,7 +255,7 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
     if (!active) return;
 #pragma unroll
     for (int j = 0; j < NMAX; ++j)
-        if (j < n) theta_out[row * n + j] = th[j];
+        if (EXACT || j < n) theta_out[row * n + j] = th[j];
     ep_out[row] = r.ep;
     eo_out[row] = r.eo;
     if (counts_out) {
@@ -265,7 +265,7 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
     if (iters_out) iters_out[row] = k;
 }
 
-template <int NMAX>
+template <int NMAX, bool EXACT>
 static cudaError_t launch_coop_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                  const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
                                  int32_t* iters, cudaStream_t s) {
@@ -274,12 +274,12 @@ static cudaError_t launch_coop_t(const DevRobot& rb, const DevCfg& c, const floa
     const size_t smem = coop_smem_bytes<NMAX>(block);
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pjik_coop<NMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_pjik_coop<NMAX, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)coop_smem_bytes<NMAX>(256));
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_pjik_coop<NMAX><<<T, block, smem, s>>>(rb, c, targets, seeds, theta, ep, eo, counts, iters);
+    k_pjik_coop<NMAX, EXACT><<<T, block, smem, s>>>(rb, c, targets, seeds, theta, ep, eo, counts, iters);
     return cudaGetLastError();
 }
 
@@ -287,9 +287,15 @@ cudaError_t launch_pjik_coop(const DevRobot& rb, const DevCfg& c, const float* t
                              const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
                              int32_t* iters, cudaStream_t s) {
     if (c.copies * c.K > 256 || 2 * c.A + 2 > 64) return cudaErrorInvalidConfiguration;
-    if (rb.n <= 8) return launch_coop_t<8>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
-    if (rb.n <= 16) return launch_coop_t<16>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
-    return launch_coop_t<32>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+    switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
+        case 7: return launch_coop_t<7, true>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+        case 8: return launch_coop_t<8, true>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+        case 14: return launch_coop_t<14, true>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+        default: break;
+    }
+    if (rb.n <= 8) return launch_coop_t<8, false>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+    if (rb.n <= 16) return launch_coop_t<16, false>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+    return launch_coop_t<32, false>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
 }
 
 }  // namespace hjcd

@@ -10,22 +10,47 @@
 // argmins, the gamma test on the composed two-joint move, and Philox
 // perturbation.  Seeding (Alg. 3 l.2-3) is fused in.  Per-seed freeze on the
 // coarse test (Alg. 3 l.14) is deterministic.
+#include <cooperative_groups.h>
+
 #include "kin.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace hjcd {
 
-template <int NMAX, bool EXACT>
+// TEXIT = false: one thread per (target, seed) anywhere in the grid; each seed
+//   freezes on its own coarse test (per-seed break).
+// TEXIT = true : the paper's stop rule ("once a seed satisfies the ...
+//   thresholds, the parallel loop is broken and all samples are returned";
+//   DESIGN.md R12b) as a deterministic lockstep: the M seeds of a target live
+//   in ONE thread-block cluster (CL CTAs x nt threads, seed m = rank * nt +
+//   threadIdx.x) and after every coarse test the cluster ORs the per-warp
+//   "converged" votes into a 3-slot flag ring in each CTA's shared memory
+//   (DSMEM stores, then barrier.cluster arrive.release / wait.acquire); all
+//   seeds of the target stop at the first iteration in which any seed passed.
+template <int NMAX, bool EXACT, bool TEXIT>
 __global__ void __launch_bounds__(128)
 k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float* __restrict__ targets, int T, const float* __restrict__ seeds,
         float* __restrict__ theta_out, float* __restrict__ cost_out, float* __restrict__ ep_out,
-        float* __restrict__ eo_out, int32_t* __restrict__ iters_out) {
+        float* __restrict__ eo_out, int32_t* __restrict__ iters_out, int CL) {
     const int M = c.M;
     const int n = rb.n;
-    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= (long long)T * M) return;
-    const int t = (int)(gid / M);
-    const int m = (int)(gid - (long long)t * M);
+    int t, m;
+    bool active = true;
+    __shared__ int s_flag[3];
+    if (TEXIT) {
+        t = (int)(blockIdx.x / (unsigned)CL);
+        m = (int)(blockIdx.x - (unsigned)t * CL) * (int)blockDim.x + (int)threadIdx.x;
+        active = m < M;
+        if (threadIdx.x < 3) s_flag[threadIdx.x] = 0;
+        cg::this_cluster().sync();   // flags initialised before any remote store
+    } else {
+        const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        if (gid >= (long long)T * M) return;
+        t = (int)(gid / M);
+        m = (int)(gid - (long long)t * M);
+    }
     const Target tg = load_target(targets + 7ll * t);
     const uint32_t tid = (uint32_t)(c.tid_offset + t);
 
@@ -34,7 +59,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     if (seeds) {
 #pragma unroll
         for (int j = 0; j < NMAX; ++j)
-            if (EXACT || j < n) th[j] = seeds[((long long)t * n + j) * M + m];
+            if (EXACT || j < n) th[j] = active ? seeds[((long long)t * n + j) * M + m] : rb.j[j].lo;
     } else {
 #pragma unroll
         for (int blk = 0; blk < (NMAX + 3) / 4; ++blk) {
@@ -67,7 +92,23 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         ep = sqrtf(dot3(rp, rp));
         eo = 2.f * fast_atan2f(sv, qr.w);              // |omega|
         // Alg. 3 l.14: coarse test (R12), checked at iteration start
-        if (ep < c.eps_p_coarse && eo < c.eps_o_coarse) break;
+        const bool conv = ep < c.eps_p_coarse && eo < c.eps_o_coarse;
+        if (TEXIT) {
+            // R12b: cluster-wide OR of the votes of iteration k (slot k % 3;
+            // slot (k + 2) % 3 is cleared after the barrier: its readers passed
+            // barrier k - 1 ... k, its next writers wait for barrier k + 1)
+            cg::cluster_group cluster = cg::this_cluster();
+            const int slot = k % 3;
+            const unsigned vote = __ballot_sync(0xffffffffu, conv && active);
+            if (vote && (threadIdx.x & 31) == 0)
+                for (int r = 0; r < CL; ++r) *cluster.map_shared_rank(&s_flag[slot], r) = 1;
+            cluster.sync();
+            const bool any = s_flag[slot] != 0;
+            if (threadIdx.x == 0) s_flag[(k + 2) % 3] = 0;
+            if (any) break;
+        } else if (conv) {
+            break;
+        }
         if (k == c.ccd_iters) break;
 
         // Eq. 10 (R2): phi = 2 atan2(|v|, w), a = v / |v|
@@ -192,6 +233,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         }
     }
 
+    if (!active) return;
 #pragma unroll
     for (int j = 0; j < NMAX; ++j)
         if (EXACT || j < n) theta_out[((long long)t * n + j) * M + m] = th[j];
@@ -202,16 +244,55 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     if (iters_out) iters_out[o] = k;
 }
 
+// seeds per CTA (nt) and CTAs per cluster (CL) of the lockstep launch:
+// 128-thread CTAs (32 for M < 128), up to 16 per cluster (non-portable size
+// above 8), so M <= 2048
+static void texit_shape(int M, int& nt, int& CL) {
+    nt = M < 128 ? (M + 31) / 32 * 32 : 128;
+    CL = (M + nt - 1) / nt;
+}
+
 template <int NMAX, bool EXACT>
 static cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                   const float* seeds, float* theta, float* cost, float* ep, float* eo,
                                   int32_t* iters, cudaStream_t s) {
-    const long long total = (long long)T * c.M;
-    const int block = 128;
-    const long long grid = (total + block - 1) / block;
+    if (!c.ccd_early_exit) {
+        const long long total = (long long)T * c.M;
+        const int block = 128;
+        const long long grid = (total + block - 1) / block;
+        if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+        k_poccd<NMAX, EXACT, false><<<(unsigned)grid, block, 0, s>>>(rb, c, targets, T, seeds, theta, cost, ep, eo,
+                                                                      iters, 1);
+        return cudaGetLastError();
+    }
+    int nt, CL;
+    texit_shape(c.M, nt, CL);
+    if (CL > 16) return cudaErrorInvalidConfiguration;
+    if (CL > 8) {
+        static bool np = false;
+        if (!np) {
+            cudaError_t e = cudaFuncSetAttribute(k_poccd<NMAX, EXACT, true>,
+                                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+            np = true;
+        }
+    }
+    const long long grid = (long long)T * CL;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-    k_poccd<NMAX, EXACT><<<(unsigned)grid, block, 0, s>>>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid, 1, 1);
+    cfg.blockDim = dim3(nt, 1, 1);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_poccd<NMAX, EXACT, true>, rb, c, targets, T, seeds, theta, cost, ep, eo,
+                              iters, CL);
 }
 
 cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,

@@ -72,19 +72,19 @@ __device__ __forceinline__ float cost_w(const float (&W)[6], const float (&rho)[
     return 0.5f * s;
 }
 
-template <int NMAX>
+template <int NMAX, bool EXACT = false>
 __device__ __forceinline__ Resid eval_at(const DevRobot& rb, const Target& tg, const float (&th)[NMAX]) {
     float3 P[NMAX], Z[NMAX];   // unused (FRAMES = false), eliminated
     float3 pe;
     Quat qe;
-    fk<NMAX, false>(rb, th, P, Z, pe, qe);
+    fk<NMAX, false, EXACT>(rb, th, P, Z, pe, qe);
     return residual(tg, pe, qe);
 }
 
 // ---- LM direction (Eq. 12 via push-through, K4): A = W G W + lambda I,
 //      G_ik = sum_j J_ij J_kj / D_j; y = A^-1 W rho; dth_j = -(sum_i J_ij W_i y_i) / D_j,
 //      then the element-wise trust-region clamp (Alg. 4 l.6, R21)
-template <int NMAX>
+template <int NMAX, bool EXACT = false>
 __device__ __forceinline__ bool lm_direction(const DevRobot& rb, const DevCfg& c, const float3 (&Jp)[NMAX],
                                              const float3 (&Jo)[NMAX], const float (&invD)[NMAX],
                                              const float (&W)[6], const float (&rho)[6], float (&dth)[NMAX]) {
@@ -97,7 +97,7 @@ __device__ __forceinline__ bool lm_direction(const DevRobot& rb, const DevCfg& c
             float s = 0.f;
 #pragma unroll
             for (int j = 0; j < NMAX; ++j)
-                if (j < n) s += jrow(Jp[j], Jo[j], i) * jrow(Jp[j], Jo[j], kk) * invD[j];
+                if (EXACT || j < n) s += jrow(Jp[j], Jo[j], i) * jrow(Jp[j], Jo[j], kk) * invD[j];
             A[i * (i + 1) / 2 + kk] = W[i] * W[kk] * s + (i == kk ? c.lambda : 0.f);
         }
     float y[6];
@@ -108,7 +108,7 @@ __device__ __forceinline__ bool lm_direction(const DevRobot& rb, const DevCfg& c
     for (int i = 0; i < 6; ++i) y[i] *= W[i];
 #pragma unroll
     for (int j = 0; j < NMAX; ++j) {
-        if (j < n) {
+        if (EXACT || j < n) {
             const float s = Jp[j].x * y[0] + Jp[j].y * y[1] + Jp[j].z * y[2] + Jo[j].x * y[3] +
                             Jo[j].y * y[4] + Jo[j].z * y[5];
             dth[j] = clampf(-s * invD[j], -c.R, c.R);
@@ -119,7 +119,7 @@ __device__ __forceinline__ bool lm_direction(const DevRobot& rb, const DevCfg& c
 
 // ---- dogleg direction (Eqs. 14-15, R23): GD = -alpha_c J^T rho (Cauchy),
 //      GN = -J^T (J J^T + d_floor I)^-1 rho, smallest tau in [0,1] with |dth(tau)| <= R
-template <int NMAX>
+template <int NMAX, bool EXACT = false>
 __device__ __forceinline__ bool dogleg_direction(const DevRobot& rb, const DevCfg& c, const float3 (&Jp)[NMAX],
                                                  const float3 (&Jo)[NMAX], const float (&rho)[6],
                                                  float (&dth)[NMAX], float (&gn)[NMAX]) {
@@ -127,7 +127,7 @@ __device__ __forceinline__ bool dogleg_direction(const DevRobot& rb, const DevCf
     float gg = 0.f;
 #pragma unroll
     for (int j = 0; j < NMAX; ++j) {
-        if (j < n) {
+        if (EXACT || j < n) {
             dth[j] = Jp[j].x * rho[0] + Jp[j].y * rho[1] + Jp[j].z * rho[2] + Jo[j].x * rho[3] +
                      Jo[j].y * rho[4] + Jo[j].z * rho[5];   // g0 = J^T rho
             gg += dth[j] * dth[j];
@@ -139,7 +139,7 @@ __device__ __forceinline__ bool dogleg_direction(const DevRobot& rb, const DevCf
         float s = 0.f;
 #pragma unroll
         for (int j = 0; j < NMAX; ++j)
-            if (j < n) s += jrow(Jp[j], Jo[j], i) * dth[j];
+            if (EXACT || j < n) s += jrow(Jp[j], Jo[j], i) * dth[j];
         jg2 += s * s;
     }
     if (!(gg > 0.f) || !(jg2 > 0.f)) return false;
@@ -152,7 +152,7 @@ __device__ __forceinline__ bool dogleg_direction(const DevRobot& rb, const DevCf
             float s = 0.f;
 #pragma unroll
             for (int j = 0; j < NMAX; ++j)
-                if (j < n) s += jrow(Jp[j], Jo[j], i) * jrow(Jp[j], Jo[j], kk);
+                if (EXACT || j < n) s += jrow(Jp[j], Jo[j], i) * jrow(Jp[j], Jo[j], kk);
             A[i * (i + 1) / 2 + kk] = s + (i == kk ? c.d_floor : 0.f);
         }
     float y[6];
@@ -162,7 +162,7 @@ __device__ __forceinline__ bool dogleg_direction(const DevRobot& rb, const DevCf
     float ngn2 = 0.f, ngd2 = 0.f;
 #pragma unroll
     for (int j = 0; j < NMAX; ++j) {
-        if (j < n) {
+        if (EXACT || j < n) {
             gn[j] = -(Jp[j].x * y[0] + Jp[j].y * y[1] + Jp[j].z * y[2] + Jo[j].x * y[3] + Jo[j].y * y[4] +
                       Jo[j].z * y[5]);
             dth[j] = -alpha_c * dth[j];   // GD
@@ -178,7 +178,7 @@ __device__ __forceinline__ bool dogleg_direction(const DevRobot& rb, const DevCf
         float qa = 0.f, qb = 0.f;
 #pragma unroll
         for (int j = 0; j < NMAX; ++j) {
-            if (j < n) {
+            if (EXACT || j < n) {
                 const float d = dth[j] - gn[j];
                 qa += d * d;
                 qb += 2.f * gn[j] * d;
@@ -196,13 +196,13 @@ __device__ __forceinline__ bool dogleg_direction(const DevRobot& rb, const DevCf
     }
 #pragma unroll
     for (int j = 0; j < NMAX; ++j)
-        if (j < n) dth[j] = wgd * dth[j] + wgn * gn[j];
+        if (EXACT || j < n) dth[j] = wgd * dth[j] + wgn * gn[j];
     return true;
 }
 
 // ---- single-coordinate direction (Eq. 16, R24): i* = argmax |g_i|, g = J^T W^2 rho,
 //      step -sign(g_i*) min(|g_i*|, R) on i* only
-template <int NMAX>
+template <int NMAX, bool EXACT = false>
 __device__ __forceinline__ bool single_coord_direction(const DevRobot& rb, const DevCfg& c,
                                                        const float3 (&Jp)[NMAX], const float3 (&Jo)[NMAX],
                                                        const float (&W)[6], const float (&rho)[6],
@@ -215,7 +215,7 @@ __device__ __forceinline__ bool single_coord_direction(const DevRobot& rb, const
     float gbest = 0.f, gabs = -1.f;
 #pragma unroll
     for (int j = 0; j < NMAX; ++j) {
-        if (j < n) {
+        if (EXACT || j < n) {
             const float g = Jp[j].x * wr[0] + Jp[j].y * wr[1] + Jp[j].z * wr[2] + Jo[j].x * wr[3] +
                             Jo[j].y * wr[4] + Jo[j].z * wr[5];
             if (fabsf(g) > gabs) { gabs = fabsf(g); gbest = g; ist = j; }

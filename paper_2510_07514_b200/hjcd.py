@@ -43,7 +43,7 @@ class hjcd_joint(C.Structure):
 class hjcd_config(C.Structure):
     _fields_ = [("M", C.c_int32), ("K", C.c_int32), ("B", C.c_int32),
                 ("ccd_iters", C.c_int32), ("lm_iters", C.c_int32),
-                ("target_early_exit", C.c_int32),
+                ("target_early_exit", C.c_int32), ("ccd_early_exit", C.c_int32),
                 ("eps_p_coarse", C.c_float), ("eps_o_coarse", C.c_float),
                 ("eps_p_fine", C.c_float), ("eps_o_fine", C.c_float),
                 ("gamma", C.c_float), ("delta0", C.c_float), ("delta_rho", C.c_float),

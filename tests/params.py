@@ -16,6 +16,7 @@ DEFAULTS = dict(
     tau_deg=1e-5,                                            # R4
     rng_seed=0, repl_noise_all=0,
     target_early_exit=1,                                     # R26b
+    ccd_early_exit=1,                                        # R12b
 )
 
 

@@ -85,7 +85,8 @@ def test_config_and_workspace_validation(hjcd_lib):
     # theta1 28 MB + cost 4 MB + seeds 2.8 MB + ep/eo 0.8 MB
     assert 35e6 < n.value < 37e6 and n.value % 256 == 0
     for bad in (dict(K=2000), dict(K=200, B=100), dict(M=0), dict(beta=1.0), dict(lambda_=0.0),
-                dict(target_early_exit=2), dict(K=1, B=300), dict(lm_iters=-1)):
+                dict(target_early_exit=2), dict(K=1, B=300), dict(lm_iters=-1),
+                dict(ccd_early_exit=2), dict(M=3000, K=50, B=100)):
         cb = hjcd_lib.default_config(**bad)
         st = L.hjcd_workspace_size(r.handle, 10, C.byref(cb), C.byref(n))
         assert st in (1, 2), bad

@@ -98,7 +98,7 @@ def poccd_compare(hjcd_lib, cuda, ch, p, tg, seeds=None):
     ("fetch", 4, 0.85), ("fetch", 64, 0.1), ("panda_x14", 16, 0.5)])
 def test_poccd_per_seed_parity(hjcd_lib, cuda, name, iters, floor):
     ch = inputs.robot(name)
-    p = params(M=300, ccd_iters=iters)
+    p = params(M=300, ccd_iters=iters, ccd_early_exit=0)
     tg, _ = targets_for(ch, 4)
     agree, clean, ref, _ = poccd_compare(hjcd_lib, cuda, ch, p, tg)
     bad = clean & ~agree
@@ -109,12 +109,58 @@ def test_poccd_per_seed_parity(hjcd_lib, cuda, name, iters, floor):
 def test_poccd_explicit_seeds_and_ragged(hjcd_lib, cuda):
     ch = inputs.fetch_like8()
     M = 131   # ragged vs the 128-thread block
-    p = params(M=M, ccd_iters=8)
+    p = params(M=M, ccd_iters=8, ccd_early_exit=0)
     tg, _ = targets_for(ch, 3)
     seeds = np.stack([inputs.uniform_configs(ch, M, seed=40 + t).T for t in range(3)]).astype(np.float32)
     agree, clean, ref, _ = poccd_compare(hjcd_lib, cuda, ch, p, tg, seeds)
     assert not (clean & ~agree).any()
     assert agree.mean() > 0.8
+
+
+@pytest.mark.parametrize("name,M,Tn", [("panda", 1000, 12), ("fetch", 131, 16), ("panda", 64, 16),
+                                       ("panda_x14", 300, 8)])
+def test_poccd_target_early_exit_parity(hjcd_lib, cuda, name, M, Tn):
+    # R12b: the M seeds of a target (one thread-block cluster, ragged
+    # across CTAs) stop together at k*; where the GPU and the oracle stop at the
+    # same k*, clean seeds agree; k* agrees on most targets
+    ch = inputs.robot(name)
+    p = params(M=M, ccd_early_exit=1)
+    tg, _ = targets_for(ch, Tn, start=60)
+    agree, clean, ref, out = poccd_compare(hjcd_lib, cuda, ch, p, tg)
+    gi, ri = N(out["iters"]), ref["iters"]
+    assert np.all(gi == gi[:, :1]) and np.all(ri == ri[:, :1])
+    same = gi[:, 0] == ri[:, 0]
+    assert same.mean() >= 0.75, (gi[:, 0], ri[:, 0])
+    assert not (clean[same] & ~agree[same]).any()
+    # a target that stopped early has a seed that passed the coarse test
+    ep, eo = N(out["ep"]), N(out["eo"])
+    early = gi[:, 0] < p["ccd_iters"]
+    assert np.all(((ep < p["eps_p_coarse"]) & (eo < p["eps_o_coarse"])).any(axis=1)[early])
+
+
+@pytest.mark.parametrize("name,M", [("panda", 1000), ("fetch", 2000)])
+def test_poccd_lockstep_is_truncated_per_seed_run(hjcd_lib, cuda, name, M):
+    # the cluster-lockstep kernel must equal the per-seed kernel run for exactly
+    # k* iterations (both on the GPU), k* = min over seeds of the per-seed
+    # convergence iteration; M = 2000 exercises a 16-CTA (non-portable) cluster
+    ch = inputs.robot(name)
+    rb = hjcd_lib.Robot(ch)
+    Tn = 6
+    tg, _ = targets_for(ch, Tn, start=7)
+    p = params(M=M)
+    ex = hjcd_lib.poccd(rb, hjcd_lib.config_from_params(p), T(tg, cuda))
+    free = hjcd_lib.poccd(rb, hjcd_lib.config_from_params(dict(p, ccd_early_exit=0)), T(tg, cuda))
+    fi, fe, fo = N(free["iters"]), N(free["ep"]), N(free["eo"])
+    conv = (fe < p["eps_p_coarse"]) & (fo < p["eps_o_coarse"])
+    kref = np.where(conv, fi, p["ccd_iters"]).min(1)
+    kst = N(ex["iters"])[:, 0]
+    # two instantiations of the same arithmetic: FMA contraction may differ by an ulp
+    assert (kst == kref).mean() >= 0.8, (kst, kref)
+    for t in range(Tn):
+        q = dict(p, ccd_early_exit=0, ccd_iters=int(kst[t]), target_index_offset=t)
+        seq = hjcd_lib.poccd(rb, hjcd_lib.config_from_params(q), T(tg[t:t + 1], cuda))
+        d = np.abs(N(seq["theta"])[0] - N(ex["theta"])[t]).max(axis=0)
+        assert (d < 1e-4).mean() >= 0.97, (t, (d < 1e-4).mean())
 
 
 def test_poccd_seeded_on_answer(hjcd_lib, cuda):

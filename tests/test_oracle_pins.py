@@ -431,7 +431,7 @@ def test_poccd_gamma_infinite_is_random_walk():
 
 def test_poccd_invariants():
     ch = inputs.fetch_like8()
-    p = params(M=64, ccd_iters=32)
+    p = params(M=64, ccd_iters=32, ccd_early_exit=0)
     tgt = oracle.fk(ch, inputs.halton_configs(ch, 2)).astype(np.float32)
     r = oracle.po_ccd(ch, p, tgt)
     lo, hi = ch.limits()
@@ -444,8 +444,30 @@ def test_poccd_invariants():
             q = oracle.fk(ch, r["theta"][t, :, m][None])[0]
             assert abs(np.linalg.norm(q[:3] - tgt[t, :3]) - r["ep"][t, m]) < 1e-12
     # more iterations never hurt the best seed much; error falls from the seeds
-    r0 = oracle.po_ccd(ch, params(M=64, ccd_iters=0), tgt)
+    r0 = oracle.po_ccd(ch, params(M=64, ccd_iters=0, ccd_early_exit=0), tgt)
     assert np.median(r["ep"]) < np.median(r0["ep"])
+
+
+def test_poccd_target_early_exit_is_lockstep_truncation():
+    # R12b: with ccd_early_exit every seed of a target stops after k*
+    # iterations, k* = the first iteration at which any seed passes the coarse
+    # test; each seed's state equals its own per-seed trajectory truncated at k*
+    for name in ("panda", "fetch"):
+        ch = inputs.robot(name)
+        M, Tn = 48, 3
+        tg = oracle.fk(ch, inputs.halton_configs(ch, Tn)).astype(np.float32)
+        free = oracle.po_ccd(ch, params(M=M, ccd_early_exit=0), tg)
+        ex = oracle.po_ccd(ch, params(M=M, ccd_early_exit=1), tg)
+        for t in range(Tn):
+            conv = (free["ep"][t] < 5e-3) & (free["eo"][t] < 5e-2)
+            kstar = free["iters"][t][conv].min() if conv.any() else 64
+            assert np.all(ex["iters"][t] == kstar)
+            trunc = oracle.po_ccd(ch, params(M=M, ccd_early_exit=0, ccd_iters=int(kstar)), tg[t:t + 1],
+                                  tid_offset=t)
+            assert np.array_equal(trunc["theta"][0], ex["theta"][t])
+            assert np.array_equal(trunc["ep"][0], ex["ep"][t])
+            if conv.any():
+                assert np.any((ex["ep"][t] < 5e-3) & (ex["eo"][t] < 5e-2))
 
 
 # ---------------------------------------------------------------- P15 PJ-IK special cases
