@@ -200,6 +200,7 @@ def main():
     ap.add_argument("--impl", default="hjcd", choices=["hjcd", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the latency-vs-batch sweep")
     ap.add_argument("--targets", type=int, default=None, help="override targets per GPU")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -234,16 +235,24 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     ws = hjcd.Workspace()
 
-    def step():
-        return solve_distributed(robot, targets, cfg, workspace=ws) if world > 1 else \
-            hjcd.solve(robot, targets, cfg, workspace=ws)
+    KNAMES = ("k_poccd", "k_select_replicate", "k_pjik", "k_select_best")
+
+    def step(events=None):
+        fn = (lambda r, t, c: hjcd.solve(r, t, c, workspace=ws, events=events))
+        return solve_distributed(robot, targets, cfg, solve_fn=fn) if world > 1 else fn(robot, targets, cfg)
 
     for _ in range(args.warmup):
         out = step()
     torch.cuda.synchronize()
 
-    # ---------------- timed region: K steps of the public API, CUDA events per step
+    # ---------------- timed region: K steps of the public API, CUDA events per
+    # step (ours) and at the kernel boundaries inside each step (recorded by the
+    # library on the same stream: hjcd_solve_timed)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    for ks in kev:
+        for e in ks:
+            e.record(stream)      # materialise the events before the timed region
     clk = Clocks(local, os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv") if os.path.isdir(
         os.path.join(ROOT, "gpurun_out")) else f"/tmp/hjcd_clocks_rank{rank}.csv")
     if world > 1:
@@ -253,7 +262,7 @@ def main():
         for s in range(args.steps):
             flush.fill_(s & 0xFF)            # L2 flush between steps (outside the events)
             evs[s][0].record(stream)
-            out = step()
+            out = step(kev[s])
             evs[s][1].record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -271,40 +280,18 @@ def main():
     q, pe, oe, st = out
     st_np = st.cpu().numpy()
     succ = float(np.mean(st_np <= 1))
+    kmean = {k: statistics.mean(ks[i].elapsed_time(ks[i + 1]) for ks in kev) for i, k in enumerate(KNAMES)}
 
-    # ---------------- per-kernel breakdown (same kernels, staged entry points;
-    # each stage timed alone: flush, sync, event, launch, event)
-    kern = {"k_poccd": [], "k_select_replicate": [], "k_pjik": [], "k_select_best": []}
-    nb = max(3, min(args.steps, 10))
-
-    def timed(fn):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        flush.fill_(7)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        r = fn()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        return r, e0.elapsed_time(e1)
-
-    # untimed pass first: the stage entry points allocate their outputs, and the
-    # caching allocator's first cudaMalloc must not land inside an event pair
+    # ---------------- algorithmic work of the timed launches: the staged entry
+    # points run the same kernels on the same inputs (deterministic), untimed,
+    # to count the iterations each seed executed
     o1 = hjcd.poccd(robot, cfg, targets)
     seeds, _ = hjcd.select_replicate(robot, cfg, o1["cost"], o1["theta"])
     o2 = hjcd.pjik(robot, cfg, targets, seeds)
-    hjcd.select_best(robot, cfg, targets, o2["theta"], o2["ep"], o2["eo"])
-    for s in range(nb):
-        o1, t1 = timed(lambda: hjcd.poccd(robot, cfg, targets))
-        (seeds, _), t2 = timed(lambda: hjcd.select_replicate(robot, cfg, o1["cost"], o1["theta"]))
-        o2, t3 = timed(lambda: hjcd.pjik(robot, cfg, targets, seeds))
-        _, t4 = timed(lambda: hjcd.select_best(robot, cfg, targets, o2["theta"], o2["ep"], o2["eo"]))
-        for k, v in zip(kern, (t1, t2, t3, t4)):
-            kern[k].append(v)
     iters_sum = int(o1["iters"].sum().item())
     used = (B // K) * K
     pj_iters_sum = int(o2["iters"][:, :used].sum().item())
     kstar = o2["iters"][:, 0].float()
-    kmean = {k: statistics.mean(v) for k, v in kern.items()}
     pk = peaks()
     peak_tf, mhz, peak_src = fp32_peak_tflops(pk)
     seeds_total = Tg * M
@@ -322,16 +309,43 @@ def main():
                 "peak_source": f"148 SM x 128 FP32 lanes x 2 x {mhz:.0f} MHz ({peak_src})",
                 "algorithmic_flops_per_launch": poccd_flops,
                 "unit_flops": f"{flops_poccd_iter(n)} per seed-iteration + {flops_poccd_final(n)} per seed",
-                "kernel_ms": kmean,
+                "kernel_ms": kmean, "kernel_ms_source": "library events at the stage boundaries of every timed step",
                 "share_of_step": {k: v / sum(kmean.values()) for k, v in kmean.items()},
                 "k_pjik": {"achieved": pjik_flops / (kmean["k_pjik"] / 1e3) / 1e12,
-                           "frac": pjik_flops / (kmean["k_pjik"] / 1e3) / 1e12 / peak_tf},
+                           "frac": pjik_flops / (kmean["k_pjik"] / 1e3) / 1e12 / peak_tf,
+                           "bound_note": "latency of the slowest target (per-target stop rule), not ALU"},
                 "poccd_mean_iters": iters_sum / seeds_total,
                 "pjik_kstar": {"mean": float(kstar.mean()), "p50": float(kstar.median()),
                                "p99": float(torch.quantile(kstar, 0.99)), "max": float(kstar.max()),
                                "frac_at_budget": float((kstar >= cfg.lm_iters).float().mean())},
                 "status_hist": [int((st == i).sum()) for i in range(4)],
                 "pjik_mean_iters": pj_iters_sum / (Tg * (B // K) * K)}
+
+    # ---------------- latency vs batch (BASELINE metric "p50 latency vs batch"):
+    # one hjcd_solve of T targets, same robot and config, device-resident I/O
+    sweep = []
+    if not args.no_sweep and world == 1:
+        for Ts in (1, 10, 100, 1000, 10000):
+            ths = torch.from_numpy(inputs.halton_configs(chain, Ts, start=50000).astype(np.float32)).to(dev)
+            tgs = hjcd.fk(robot, ths).contiguous()
+            c2 = hjcd.default_config(M=M, K=K, B=B, target_index_offset=50000)
+            sws = hjcd.Workspace()
+            for _ in range(2):
+                hjcd.solve(robot, tgs, c2, workspace=sws)
+            reps = 20 if Ts <= 1000 else 5
+            lat = []
+            for _ in range(reps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                r = hjcd.solve(robot, tgs, c2, workspace=sws)
+                b.record(stream)
+                b.synchronize()
+                lat.append(a.elapsed_time(b))
+            lat.sort()
+            sweep.append({"targets": Ts, "p50_ms": lat[len(lat) // 2],
+                          "p99_ms": lat[min(len(lat) - 1, int(math.ceil(0.99 * len(lat))) - 1)],
+                          "solves_per_s": Ts / (lat[len(lat) // 2] / 1e3),
+                          "success": float((r[3] <= 1).float().mean())})
 
     # ---------------- end to end through the C ABI with host buffers
     tg_host = targets.cpu().pin_memory()
@@ -371,7 +385,7 @@ def main():
                "p50_ms": srt[len(srt) // 2], "p99_ms": srt[min(len(srt) - 1, int(math.ceil(0.99 * len(srt))) - 1)],
                "latency_note": "p50/p99 of the per-step batch latency (one hjcd_solve of all targets)",
                "success_rate_1mm_1deg": succ,
-               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "latency_vs_batch": sweep,
                "gpu_launches": 4 * args.steps, "clocks": clk.summary(),
                "paper_context": "RTX 4060 Laptop, Panda M=1000: 7.53 ms per target (133 targets/s), PAPER.md P:355"}
         print(json.dumps(res))

@@ -147,6 +147,15 @@ hjcd_status hjcd_solve(const hjcd_robot* r, const hjcd_config* c, const float* t
                        float* q_out, float* pos_err, float* ori_err, int32_t* status,
                        void* workspace, size_t workspace_bytes, hjcd_stream_t stream);
 
+/* hjcd_solve that also records stage boundaries for live per-kernel timing:
+ * events = NULL or an array of 5 caller-created CUDA events (cudaEvent_t,
+ * created with timing enabled), recorded on `stream` before PO-CCD, after
+ * PO-CCD, after top-K/replicate, after PJ-IK and after best-select. */
+hjcd_status hjcd_solve_timed(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                             float* q_out, float* pos_err, float* ori_err, int32_t* status,
+                             void* workspace, size_t workspace_bytes, hjcd_stream_t stream,
+                             void* const* events);
+
 /* The same with HOST buffers (same shapes): copies targets host->device,
  * solves, copies results device->host, and synchronises `stream` before
  * returning.  workspace: device, >= hjcd_workspace_size_host bytes. */

@@ -294,6 +294,13 @@ hjcd_status hjcd_workspace_size_host(const hjcd_robot* r, int32_t T, const hjcd_
 hjcd_status hjcd_solve(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
                        float* q_out, float* pos_err, float* ori_err, int32_t* status, void* workspace,
                        size_t workspace_bytes, hjcd_stream_t stream) {
+    return hjcd_solve_timed(r, c, targets, T, q_out, pos_err, ori_err, status, workspace, workspace_bytes,
+                            stream, nullptr);
+}
+
+hjcd_status hjcd_solve_timed(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                             float* q_out, float* pos_err, float* ori_err, int32_t* status, void* workspace,
+                             size_t workspace_bytes, hjcd_stream_t stream, void* const* events) {
     if (!r || !c || !targets || T < 1 || !q_out || !pos_err || !ori_err || !status || !workspace)
         return HJCD_E_INVALID_ARG;
     DevCfg d;
@@ -311,18 +318,26 @@ hjcd_status hjcd_solve(const hjcd_robot* r, const hjcd_config* c, const float* t
     float* eo2 = (float*)(ws + L.eo2);
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e;
+    auto mark = [&](int i) -> cudaError_t {
+        return (events && events[i]) ? cudaEventRecord((cudaEvent_t)events[i], s) : cudaSuccess;
+    };
+    if ((e = mark(0)) != cudaSuccess) return cuda_fail(e);
     // Alg. 2 l.1: PO-CCD over M seeds per target
-    if ((e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s)) != cudaSuccess)
+    if ((e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s)) != cudaSuccess ||
+        (e = mark(1)) != cudaSuccess)
         return cuda_fail(e);
     // Alg. 2 l.2-8: top-K + replicate
-    if ((e = launch_select_replicate(r->dev, d, cost1, theta1, T, seeds2, nullptr, s)) != cudaSuccess)
+    if ((e = launch_select_replicate(r->dev, d, cost1, theta1, T, seeds2, nullptr, s)) != cudaSuccess ||
+        (e = mark(2)) != cudaSuccess)
         return cuda_fail(e);
     // Alg. 2 l.9 / Alg. 4: PJ-IK, in place on the replicated seeds
-    if ((e = launch_pjik(r->dev, d, targets, T, seeds2, seeds2, ep2, eo2, nullptr, nullptr, s)) != cudaSuccess)
+    if ((e = launch_pjik(r->dev, d, targets, T, seeds2, seeds2, ep2, eo2, nullptr, nullptr, s)) != cudaSuccess ||
+        (e = mark(3)) != cudaSuccess)
         return cuda_fail(e);
     // Alg. 2 l.10: best of B
     if ((e = launch_select_best(r->dev, d, targets, T, seeds2, ep2, eo2, q_out, pos_err, ori_err, status, s)) !=
-        cudaSuccess)
+            cudaSuccess ||
+        (e = mark(4)) != cudaSuccess)
         return cuda_fail(e);
     return HJCD_OK;
 }

@@ -24,7 +24,7 @@ TARGET_CONVERGED, TARGET_SUCCESS, TARGET_NOT_CONVERGED, TARGET_INVALID = 0, 1, 2
 EXPORTS = [
     "hjcd_robot_create", "hjcd_robot_extend", "hjcd_robot_destroy", "hjcd_robot_dof",
     "hjcd_robot_limits", "hjcd_config_default", "hjcd_workspace_size",
-    "hjcd_workspace_size_host", "hjcd_solve", "hjcd_solve_host", "hjcd_fk", "hjcd_poccd",
+    "hjcd_workspace_size_host", "hjcd_solve", "hjcd_solve_timed", "hjcd_solve_host", "hjcd_fk", "hjcd_poccd",
     "hjcd_select_replicate", "hjcd_pjik", "hjcd_select_best", "hjcd_status_string",
     "hjcd_last_cuda_error", "hjcd_version",
 ]
@@ -77,6 +77,7 @@ def lib():
         L.hjcd_workspace_size.argtypes = [P, i32, P, C.POINTER(sz)]
         L.hjcd_workspace_size_host.argtypes = [P, i32, P, C.POINTER(sz)]
         L.hjcd_solve.argtypes = [P, P, P, i32, P, P, P, P, P, sz, P]
+        L.hjcd_solve_timed.argtypes = [P, P, P, i32, P, P, P, P, P, sz, P, P]
         L.hjcd_solve_host.argtypes = [P, P, P, i32, P, P, P, P, P, sz, P]
         L.hjcd_fk.argtypes = [P, P, i32, P, P, P]
         L.hjcd_poccd.argtypes = [P, P, P, i32, P, P, P, P, P, P, P]
@@ -232,9 +233,11 @@ def _ws_for(device, nbytes, ws: Optional[Workspace]):
 
 # ---------------------------------------------------------------- API
 def solve(robot: Robot, targets, cfg: Optional[hjcd_config] = None, out=None,
-          workspace: Optional[Workspace] = None, stream=None):
+          workspace: Optional[Workspace] = None, stream=None, events=None):
     """HJCD-IK for targets [T, 7] (cuda f32).  Returns (q [T, dof], pos_err [T],
-    ori_err [T], status [T] int32), all on the targets' device; asynchronous."""
+    ori_err [T], status [T] int32), all on the targets' device; asynchronous.
+    events: optional 5 torch.cuda.Event(enable_timing=True), recorded by the
+    library at the stage boundaries (hjcd_solve_timed)."""
     torch = _torch()
     cfg = cfg or default_config()
     T = targets.shape[0]
@@ -248,8 +251,15 @@ def solve(robot: Robot, targets, cfg: Optional[hjcd_config] = None, out=None,
     q, pe, oe, st = out
     nbytes = workspace_size(robot, T, cfg)
     ws = _ws_for(dev, nbytes, workspace)
-    _check(lib().hjcd_solve(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(q), _ptr(pe),
-                            _ptr(oe), _ptr(st), _ptr(ws), ws.numel(), _stream(stream)),
+    evp = None
+    if events is not None:
+        assert len(events) == 5
+        for ev in events:
+            if not ev.cuda_event:          # torch creates the event lazily on first record
+                ev.record()
+        evp = (C.c_void_p * 5)(*[ev.cuda_event for ev in events])
+    _check(lib().hjcd_solve_timed(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(q), _ptr(pe),
+                                  _ptr(oe), _ptr(st), _ptr(ws), ws.numel(), _stream(stream), evp),
            "hjcd_solve")
     return q, pe, oe, st
 
