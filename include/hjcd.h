@@ -102,11 +102,12 @@ hjcd_status hjcd_robot_limits(const hjcd_robot* r, float* lo, float* hi);
 /* Algorithm parameters (Alg. 2-4 headers P:175); defaults and the
  * reading behind each are in DESIGN.md "Readings" (R-numbers). */
 typedef struct {
-    int32_t M, K, B;               /* seeds, retained, polish batch: 1 <= K <= M, K <= B (Alg. 2) */
+    int32_t M, K, B;               /* seeds, retained, polish batch: 1 <= K <= M, K <= B (Alg. 2);
+                                      floor(B/K)*K <= 256 (one CTA per target in PJ-IK) */
     int32_t ccd_iters, lm_iters;   /* iteration budgets I_c (Alg. 3), I_l (Alg. 4) (R28) */
     int32_t target_early_exit;     /* PJ-IK stop rule (Alg. 4 l.18; R26b): 1 = a target stops at the
                                       first iteration in which ANY of its polish seeds passes the fine
-                                      test (deterministic, needs floor(B/K)*K <= 256); 0 = every seed
+                                      test (deterministic); 0 = every seed
                                       runs until it converges or lm_iters (per-seed freeze) */
     int32_t ccd_early_exit;        /* PO-CCD stop rule (R12b): 1 = a target's M seeds stop at the
                                       first iteration in which ANY of them passes the coarse test (one

@@ -1,0 +1,45 @@
+// dispatch.cu — picks the kernel instantiation for the robot's DoF: exact-N
+// kernels (no per-joint guards) for the benchmarked chains n = 7, 8, 14, and
+// NMAX-bounded kernels (uniform `j < n` guards) for every other n <= 32.
+#include "hjcd_internal.h"
+
+namespace hjcd {
+
+cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+                         const float* seeds, float* theta, float* cost, float* ep, float* eo,
+                         int32_t* iters, cudaStream_t s) {
+    switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
+        case 7: return launch_poccd_t<7, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+        case 8: return launch_poccd_t<8, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+        case 14: return launch_poccd_t<14, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+        default: break;
+    }
+    if (rb.n <= 8) return launch_poccd_t<8, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+    if (rb.n <= 16) return launch_poccd_t<16, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+    return launch_poccd_t<32, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+}
+
+cudaError_t launch_pjik_coop(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+                             const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
+                             int32_t* iters, cudaStream_t s) {
+    if (c.copies * c.K > 256 || 2 * c.A + 2 > 64) return cudaErrorInvalidConfiguration;
+    switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
+        case 7: return launch_coop_t<7, true>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+        case 8: return launch_coop_t<8, true>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+        case 14: return launch_coop_t<14, true>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+        default: break;
+    }
+    if (rb.n <= 8) return launch_coop_t<8, false>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+    if (rb.n <= 16) return launch_coop_t<16, false>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+    return launch_coop_t<32, false>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+}
+
+cudaError_t launch_pjik(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+                        const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
+                        int32_t* iters, cudaStream_t s) {
+    // one CTA per target, warp-cooperative cascade (pjik_coop.cuh), for both
+    // the per-target stop rule and the per-seed break
+    return launch_pjik_coop(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+}
+
+}  // namespace hjcd

@@ -167,7 +167,7 @@ hjcd_status make_cfg(const hjcd_robot* r, const hjcd_config* c, DevCfg* d) {
     if (c->M < 1 || c->K < 1 || c->B < 1 || c->K > c->M || c->K > c->B) return HJCD_E_INVALID_ARG;
     if (c->ccd_iters < 0 || c->lm_iters < 0 || c->A < 0) return HJCD_E_INVALID_ARG;
     if (c->target_early_exit != 0 && c->target_early_exit != 1) return HJCD_E_INVALID_ARG;
-    if (c->target_early_exit && ((c->B / c->K) * c->K > 256 || c->A > 31)) return HJCD_E_UNSUPPORTED;
+    if ((c->B / c->K) * c->K > 256 || c->A > 31) return HJCD_E_UNSUPPORTED;   // one CTA per target (K6)
     if (c->ccd_early_exit != 0 && c->ccd_early_exit != 1) return HJCD_E_INVALID_ARG;
     if (!(c->beta > 1.f) || !(c->lambda > 0.f) || !(c->d_floor > 0.f) || !(c->R > 0.f)) return HJCD_E_INVALID_ARG;
     if (!(c->eps_p_coarse > 0.f) || !(c->eps_o_coarse > 0.f) || !(c->eps_p_fine > 0.f) ||

@@ -47,7 +47,18 @@ struct DevCfg {
 // Philox purposes (R30)
 enum : uint32_t { P_INIT = 1, P_PERTURB = 2, P_REPL = 3, P_PJPERT = 4 };
 
-// launchers (defined in the .cu files); all asynchronous on `s`
+// per-instantiation launchers (templates in poccd.cuh / pjik_coop.cuh,
+// explicitly instantiated one or two per inst_*.cu so nvcc runs in parallel)
+template <int NMAX, bool EXACT>
+cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+                           const float* seeds, float* theta, float* cost, float* ep, float* eo,
+                           int32_t* iters, cudaStream_t s);
+template <int NMAX, bool EXACT>
+cudaError_t launch_coop_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+                          const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
+                          int32_t* iters, cudaStream_t s);
+
+// launchers (dispatch.cu, select.cu); all asynchronous on `s`
 cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, float* jac,
                       cudaStream_t s);
 cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,

@@ -183,6 +183,20 @@ __device__ __forceinline__ void fk(const DevRobot& rb, const float (&th)[NMAX], 
     qe = quat_from_rot(E);
 }
 
+// 1/x for normal positive x without the IEEE-division slow path: MUFU.RCP
+// approximation + one Newton step (|rel err| <~ 1.5 ulp)
+__device__ __forceinline__ float rcp_nr(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return fmaf(r, fmaf(-x, r, 1.f), r);
+}
+
+// 1/sqrt(x) for normal positive x: MUFU.RSQ + one Newton step
+__device__ __forceinline__ float rsqrt_nr(float x) {
+    const float r = rsqrtf(x);
+    return r * fmaf(-0.5f * x * r, r, 1.5f);
+}
+
 // atan2 on [-pi, pi] with |err| <= 3.3e-7 rad (fp32): odd minimax polynomial
 // of degree 15 for atan on [0, 1] + octant reduction (K5)
 __device__ __forceinline__ float fast_atan2f(float y, float x) {

@@ -1,6 +1,8 @@
-// pjik_coop.cu — k_pjik_coop: PJ-IK (Alg. 4) for one target per CTA
+#pragma once
+// pjik_coop.cuh — k_pjik_coop: PJ-IK (Alg. 4) for one target per CTA
 // with the per-target stop rule (Alg. 4 l.18 break; DESIGN.md
-// R26b) and WARP-COOPERATIVE line-search trials (K6).
+// R26b; or, with target_early_exit = 0, a per-seed break) and
+// WARP-COOPERATIVE line-search trials (K6).
 //
 // The B polish seeds of a target advance in lockstep (one thread per seed); the
 // CTA votes after each iteration's fine test and stops at the first iteration
@@ -69,6 +71,7 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
             float* __restrict__ theta_out, float* __restrict__ ep_out, float* __restrict__ eo_out,
             int32_t* __restrict__ counts_out, int32_t* __restrict__ iters_out) {
     extern __shared__ unsigned long long coop_raw[];
+    __shared__ int s_wtot[8];   // per-warp item totals (<= 256 threads)
     const int nt = blockDim.x;
     const CoopSmem S = coop_smem<NMAX>(coop_raw, nt);
     const int n = rb.n;
@@ -76,7 +79,6 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
     const int t = blockIdx.x;
     const int b = threadIdx.x;
     const int lane = b & 31;
-    const int wbase = b - lane;
     const bool active = b < used;
     const Target tg = load_target(targets + 7ll * t);
     const uint32_t tid = (uint32_t)(c.tid_offset + t);
@@ -89,22 +91,31 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
     int cnt[4] = {0, 0, 0, 0};
     float3 Jp[NMAX], Jo[NMAX];
     Resid r;
+    bool live = active;   // per-seed mode: cleared when this seed converges
+    int kseed = 0;
     int k;
     for (k = 0;; ++k) {
         float3 pe;
         Quat qe;
         bool conv = false;
-        if (active) {
+        if (live) {
             fk<NMAX, true, EXACT>(rb, th, Jp, Jo, pe, qe);
             r = residual(tg, pe, qe);
             conv = r.ep < c.eps_p_fine && r.eo < c.eps_o_fine;   // Alg. 4 l.18 (R26)
         }
-        if (__syncthreads_or(conv)) break;                      // R26b: target stops
+        if (c.target_early_exit) {
+            if (__syncthreads_or(conv)) break;                  // R26b: target stops
+        } else {
+            // per-seed break: a converged seed freezes (and keeps helping its
+            // warp evaluate trials); the CTA runs while any seed is live
+            if (conv) { live = false; kseed = k; }
+            if (!__syncthreads_or(live)) break;
+        }
         if (k == c.lm_iters) break;
 
         bool need = false;
         int flags = 0, items = 0;
-        if (active) {
+        if (live) {
             // ---- Eq. 7 Jacobian, W (R17), D (R20), c_W(theta), |rho|^2
 #pragma unroll
             for (int j = 0; j < NMAX; ++j) {
@@ -126,11 +137,11 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
                     if (EXACT || j < n) {
                         rn[0] += Jp[j].x * Jp[j].x; rn[1] += Jp[j].y * Jp[j].y; rn[2] += Jp[j].z * Jp[j].z;
                         rn[3] += Jo[j].x * Jo[j].x; rn[4] += Jo[j].y * Jo[j].y; rn[5] += Jo[j].z * Jo[j].z;
-                        invD[j] = 1.f / fmaxf(dot3(Jp[j], Jp[j]) + dot3(Jo[j], Jo[j]), c.d_floor);
+                        invD[j] = rcp_nr(fmaxf(dot3(Jp[j], Jp[j]) + dot3(Jo[j], Jo[j]), c.d_floor));
                     }
                 }
 #pragma unroll
-                for (int i = 0; i < 6; ++i) W[i] = (i < 3 ? c.w_p : c.w_o) / (1.f + sqrtf(rn[i]));
+                for (int i = 0; i < 6; ++i) W[i] = (i < 3 ? c.w_p : c.w_o) * rcp_nr(1.f + sqrtf(rn[i]));
             }
             const float c0 = cost_w(W, r.rho);
             // ---- own LM trial at alpha = 1 (Alg. 4 l.3-9, first element of A)
@@ -179,28 +190,36 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
             }
         }
 
-        // ---- warp-cooperative evaluation of the pending cascade trials (K6)
-        const unsigned needmask = __ballot_sync(0xffffffffu, need);
-        if (needmask) {
-            int incl = items;
+        // ---- CTA-cooperative evaluation of the pending cascade trials (K6):
+        // the items of every failing seed of the target are spread over all
+        // the CTA's lanes (the iteration lasts as long as its slowest warp)
+        int incl = items;
 #pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl += v;
-            }
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += v;
+        }
+        if (lane == 31) s_wtot[b >> 5] = incl;
+        S.ok[b] = 0ull;
+        __syncthreads();
+        int total = 0;
+        for (int w = 0; w < (nt >> 5); ++w) {
+            const int v = s_wtot[w];
+            if (w < (b >> 5)) incl += v;
+            total += v;
+        }
+        if (total > 0) {   // uniform over the CTA
             S.incl[b] = incl;
-            S.ok[b] = 0ull;
-            const int total = __shfl_sync(0xffffffffu, incl, 31);
-            __syncwarp();
-            for (int it = lane; it < total; it += 32) {
-                // owner = first lane whose inclusive prefix exceeds it
-                int lo = 0, hi = 31;
+            __syncthreads();
+            for (int it = b; it < total; it += nt) {
+                // owner = first slot whose inclusive prefix exceeds it
+                int lo = 0, hi = nt - 1;
                 while (lo < hi) {
                     const int mid = (lo + hi) >> 1;
-                    if (S.incl[wbase + mid] > it) hi = mid; else lo = mid + 1;
+                    if (S.incl[mid] > it) hi = mid; else lo = mid + 1;
                 }
-                const int o = wbase + lo;
-                const int qq = it - (lo > 0 ? S.incl[o - 1] : 0);   // item index within the owner's list
+                const int o = lo;
+                const int qq = it - (o > 0 ? S.incl[o - 1] : 0);   // item index within the owner's list
                 int kind, a;
                 decode_item(qq, S.flags[o], c.A, kind, a);
                 float alpha = 1.f;
@@ -229,7 +248,7 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
                 }
                 if (ok) atomicOr(&S.ok[o], 1ull << qq);
             }
-            __syncwarp();
+            __syncthreads();
             if (need) {
                 const unsigned long long m = S.ok[b];
                 if (m) {
@@ -248,7 +267,6 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
                     cnt[3]++;
                 }
             }
-            __syncwarp();
         }
     }
 
@@ -262,11 +280,11 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
 #pragma unroll
         for (int i = 0; i < 4; ++i) counts_out[row * 4 + i] = cnt[i];
     }
-    if (iters_out) iters_out[row] = k;
+    if (iters_out) iters_out[row] = (c.target_early_exit || live) ? k : kseed;
 }
 
 template <int NMAX, bool EXACT>
-static cudaError_t launch_coop_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+cudaError_t launch_coop_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                  const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
                                  int32_t* iters, cudaStream_t s) {
     const int used = c.copies * c.K;
@@ -281,21 +299,6 @@ static cudaError_t launch_coop_t(const DevRobot& rb, const DevCfg& c, const floa
     }
     k_pjik_coop<NMAX, EXACT><<<T, block, smem, s>>>(rb, c, targets, seeds, theta, ep, eo, counts, iters);
     return cudaGetLastError();
-}
-
-cudaError_t launch_pjik_coop(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
-                             const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
-                             int32_t* iters, cudaStream_t s) {
-    if (c.copies * c.K > 256 || 2 * c.A + 2 > 64) return cudaErrorInvalidConfiguration;
-    switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
-        case 7: return launch_coop_t<7, true>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
-        case 8: return launch_coop_t<8, true>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
-        case 14: return launch_coop_t<14, true>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
-        default: break;
-    }
-    if (rb.n <= 8) return launch_coop_t<8, false>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
-    if (rb.n <= 16) return launch_coop_t<16, false>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
-    return launch_coop_t<32, false>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
 }
 
 }  // namespace hjcd

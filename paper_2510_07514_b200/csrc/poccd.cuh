@@ -1,4 +1,5 @@
-// poccd.cu — k_poccd: stage 1 of HJCD-IK, PO-CCD (Alg. 3).
+#pragma once
+// poccd.cuh — k_poccd: stage 1 of HJCD-IK, PO-CCD (Alg. 3).
 //
 // Mapping: one thread per (target, seed).  The paper runs one block per seed
 // with two warps per joint; on B200 the per-seed work (~1.6 kflop per
@@ -247,13 +248,13 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
 // seeds per CTA (nt) and CTAs per cluster (CL) of the lockstep launch:
 // 128-thread CTAs (32 for M < 128), up to 16 per cluster (non-portable size
 // above 8), so M <= 2048
-static void texit_shape(int M, int& nt, int& CL) {
+static inline void texit_shape(int M, int& nt, int& CL) {
     nt = M < 128 ? (M + 31) / 32 * 32 : 128;
     CL = (M + nt - 1) / nt;
 }
 
 template <int NMAX, bool EXACT>
-static cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                   const float* seeds, float* theta, float* cost, float* ep, float* eo,
                                   int32_t* iters, cudaStream_t s) {
     if (!c.ccd_early_exit) {
@@ -293,20 +294,6 @@ static cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const flo
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k_poccd<NMAX, EXACT, true>, rb, c, targets, T, seeds, theta, cost, ep, eo,
                               iters, CL);
-}
-
-cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
-                         const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                         int32_t* iters, cudaStream_t s) {
-    switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
-        case 7: return launch_poccd_t<7, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-        case 8: return launch_poccd_t<8, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-        case 14: return launch_poccd_t<14, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-        default: break;
-    }
-    if (rb.n <= 8) return launch_poccd_t<8, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-    if (rb.n <= 16) return launch_poccd_t<16, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-    return launch_poccd_t<32, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
 }
 
 }  // namespace hjcd

@@ -7,9 +7,12 @@
 
 namespace hjcd {
 
-// 6x6 SPD solve by Cholesky, packed lower triangle A[i*(i+1)/2 + j].
-// Returns false if a pivot is not positive.
+// 6x6 SPD solve by Cholesky, packed lower triangle A[i*(i+1)/2 + j]; the
+// pivots are kept as reciprocals (rsqrt + Newton), so the factorisation and
+// both substitutions are multiply-only.  Returns false if a pivot is not
+// positive.
 __device__ __forceinline__ bool chol6_solve(float (&A)[21], float (&b)[6]) {
+    float id[6];
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
 #pragma unroll
@@ -18,10 +21,11 @@ __device__ __forceinline__ bool chol6_solve(float (&A)[21], float (&b)[6]) {
 #pragma unroll
             for (int k = 0; k < j; ++k) s -= A[i * (i + 1) / 2 + k] * A[j * (j + 1) / 2 + k];
             if (i == j) {
-                if (!(s > 0.f)) return false;
-                A[i * (i + 1) / 2 + i] = sqrtf(s);
+                if (!(s > 1e-30f)) return false;
+                id[i] = rsqrt_nr(s);
+                A[i * (i + 1) / 2 + i] = s * id[i];
             } else {
-                A[i * (i + 1) / 2 + j] = s / A[j * (j + 1) / 2 + j];
+                A[i * (i + 1) / 2 + j] = s * id[j];
             }
         }
     }
@@ -30,14 +34,14 @@ __device__ __forceinline__ bool chol6_solve(float (&A)[21], float (&b)[6]) {
         float s = b[i];
 #pragma unroll
         for (int k = 0; k < i; ++k) s -= A[i * (i + 1) / 2 + k] * b[k];
-        b[i] = s / A[i * (i + 1) / 2 + i];
+        b[i] = s * id[i];
     }
 #pragma unroll
     for (int i = 5; i >= 0; --i) {
         float s = b[i];
 #pragma unroll
         for (int k = i + 1; k < 6; ++k) s -= A[k * (k + 1) / 2 + i] * b[k];
-        b[i] = s / A[i * (i + 1) / 2 + i];
+        b[i] = s * id[i];
     }
     return true;
 }
@@ -56,8 +60,8 @@ __device__ __forceinline__ Resid residual(const Target& tg, float3 pe, Quat qe) 
     Resid r;
     const Quat q = quat_err(tg.q, qe);
     const float sv = sqrtf(q.x * q.x + q.y * q.y + q.z * q.z);
-    const float ang = omega_norm(sv, q.w);
-    const float scale = sv > 0.f ? ang / sv : 2.f / q.w;   // omega = scale * v (Eq. 5)
+    const float ang = 2.f * fast_atan2f(sv, q.w);           // |omega| (Eq. 5), q.w >= 0
+    const float scale = sv > 1e-30f ? ang * rcp_nr(sv) : 2.f * rcp_nr(q.w);   // omega = scale * v
     r.rho[0] = pe.x - tg.p.x; r.rho[1] = pe.y - tg.p.y; r.rho[2] = pe.z - tg.p.z;
     r.rho[3] = -scale * q.x; r.rho[4] = -scale * q.y; r.rho[5] = -scale * q.z;
     r.ep = sqrtf(r.rho[0] * r.rho[0] + r.rho[1] * r.rho[1] + r.rho[2] * r.rho[2]);
