@@ -28,15 +28,17 @@ def _newest_input() -> float:
     return max(os.path.getmtime(p) for p in paths)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_input():
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB, build_dir: str = BUILD) -> str:
+    """defines / lib / build_dir: A/B variants for experiments (-D flags)."""
+    LIBP, BUILDP = lib, build_dir
+    if not force and os.path.exists(LIBP) and os.path.getmtime(LIBP) >= _newest_input():
+        return LIBP
+    os.makedirs(BUILDP, exist_ok=True)
     objs, procs = [], []
     for src in SOURCES:   # one nvcc per translation unit, in parallel
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-        log = os.path.join(BUILD, src.replace(".cu", ".ptxas.txt"))
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(BUILDP, src.replace(".cu", ".o"))
+        log = os.path.join(BUILDP, src.replace(".cu", ".ptxas.txt"))
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append((src, log, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
@@ -51,13 +53,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
             failed.append(src)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = LIBP + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, LIBP)
+    return LIBP
 
 
 if __name__ == "__main__":

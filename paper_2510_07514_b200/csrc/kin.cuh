@@ -61,39 +61,38 @@ __device__ __forceinline__ Quat qerr_rotate(Quat q, float3 z, float c2, float s2
     return r;
 }
 
-// rotation matrix (row-major) -> unit quaternion, w >= 0 (Shepperd)
+// rotation matrix (row-major) -> unit quaternion, w >= 0 (Shepperd).  With
+// t the pivot (>= 1/4 in the chosen branch), s = 2 sqrt(t) and 1/s =
+// rsqrt(t)/2, so no division is needed.
 __device__ __forceinline__ Quat quat_from_rot(const float R[9]) {
     float tr = R[0] + R[4] + R[8];
     Quat q;
     if (tr > 0.f) {
-        float s = sqrtf(tr + 1.f) * 2.f;
-        float is = 1.f / s;
-        q.w = 0.25f * s;
+        const float t = tr + 1.f, r = rsqrtf(t), is = 0.5f * r;
+        q.w = 0.5f * t * r;
         q.x = (R[7] - R[5]) * is;
         q.y = (R[2] - R[6]) * is;
         q.z = (R[3] - R[1]) * is;
     } else if (R[0] > R[4] && R[0] > R[8]) {
-        float s = sqrtf(1.f + R[0] - R[4] - R[8]) * 2.f;
-        float is = 1.f / s;
+        const float t = 1.f + R[0] - R[4] - R[8], r = rsqrtf(t), is = 0.5f * r;
         q.w = (R[7] - R[5]) * is;
-        q.x = 0.25f * s;
+        q.x = 0.5f * t * r;
         q.y = (R[1] + R[3]) * is;
         q.z = (R[2] + R[6]) * is;
     } else if (R[4] > R[8]) {
-        float s = sqrtf(1.f + R[4] - R[0] - R[8]) * 2.f;
-        float is = 1.f / s;
+        const float t = 1.f + R[4] - R[0] - R[8], r = rsqrtf(t), is = 0.5f * r;
         q.w = (R[2] - R[6]) * is;
         q.x = (R[1] + R[3]) * is;
-        q.y = 0.25f * s;
+        q.y = 0.5f * t * r;
         q.z = (R[5] + R[7]) * is;
     } else {
-        float s = sqrtf(1.f + R[8] - R[0] - R[4]) * 2.f;
-        float is = 1.f / s;
+        const float t = 1.f + R[8] - R[0] - R[4], r = rsqrtf(t), is = 0.5f * r;
         q.w = (R[3] - R[1]) * is;
         q.x = (R[2] + R[6]) * is;
         q.y = (R[5] + R[7]) * is;
-        q.z = 0.25f * s;
+        q.z = 0.5f * t * r;
     }
+    // renormalise (absorbs the rsqrt approximation and FK rounding)
     float inv = rsqrtf(q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z);
     if (q.w < 0.f) inv = -inv;
     q.w *= inv; q.x *= inv; q.y *= inv; q.z *= inv;
@@ -260,26 +259,39 @@ __device__ __forceinline__ uint4 draw(const DevCfg& c, uint32_t tid, uint32_t si
 // ((x >> 9) + 0.5) * 2^-23: exact in fp32, in (0, 1)
 __device__ __forceinline__ float u01(uint32_t x) { return ((float)(x >> 9) + 0.5f) * 1.1920928955078125e-07f; }
 
-// 4 standard normals from one Philox block: Box-Muller on (u0,u1), (u2,u3)
+// 4 standard normals from one Philox block: Box-Muller on (u0,u1), (u2,u3).
+// FAST (coarse stage): SFU log2 / sincos (|rel err| ~1e-6 on each normal,
+// i.e. ~5e-8 rad on a sigma = 0.05 perturbation, far below the coarse
+// tolerance); otherwise the accurate library functions.
+template <bool FAST = false>
 __device__ __forceinline__ void normals4(uint4 r, float g[4]) {
     float u0 = u01(r.x), u1 = u01(r.y), u2 = u01(r.z), u3 = u01(r.w);
-    float ra = sqrtf(-2.f * logf(u0)), rb2 = sqrtf(-2.f * logf(u2));
-    float s, c;
-    sincospif(2.f * u1, &s, &c);
-    g[0] = ra * c; g[1] = ra * s;
-    sincospif(2.f * u3, &s, &c);
-    g[2] = rb2 * c; g[3] = rb2 * s;
+    if (FAST) {
+        const float ra = sqrtf(-1.38629436f * __log2f(u0)), rb2 = sqrtf(-1.38629436f * __log2f(u2));
+        float s, c;   // sin/cos(2 pi u - pi) = -sin/-cos(2 pi u), argument in (-pi, pi)
+        __sincosf(fmaf(6.28318531f, u1, -3.14159265f), &s, &c);
+        g[0] = -ra * c; g[1] = -ra * s;
+        __sincosf(fmaf(6.28318531f, u3, -3.14159265f), &s, &c);
+        g[2] = -rb2 * c; g[3] = -rb2 * s;
+    } else {
+        float ra = sqrtf(-2.f * logf(u0)), rb2 = sqrtf(-2.f * logf(u2));
+        float s, c;
+        sincospif(2.f * u1, &s, &c);
+        g[0] = ra * c; g[1] = ra * s;
+        sincospif(2.f * u3, &s, &c);
+        g[2] = rb2 * c; g[3] = rb2 * s;
+    }
 }
 
 // theta <- clamp(theta + sigma * N(0, I)), stream (tid, sid, purpose, iter)
-template <int NMAX, bool EXACT = false>
+template <int NMAX, bool EXACT = false, bool FAST = false>
 __device__ __forceinline__ void perturb(const DevRobot& rb, const DevCfg& c, float (&th)[NMAX], float sigma,
                                         uint32_t tid, uint32_t sid, uint32_t purpose, uint32_t iter) {
 #pragma unroll
     for (int blk = 0; blk < (NMAX + 3) / 4; ++blk) {
         if (EXACT || 4 * blk < rb.n) {
             float g[4];
-            normals4(draw(c, tid, sid, purpose, iter, blk), g);
+            normals4<FAST>(draw(c, tid, sid, purpose, iter, blk), g);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 int j = 4 * blk + e;

@@ -30,7 +30,10 @@ namespace hjcd {
 //   (DSMEM stores, then barrier.cluster arrive.release / wait.acquire); all
 //   seeds of the target stop at the first iteration in which any seed passed.
 template <int NMAX, bool EXACT, bool TEXIT>
-__global__ void __launch_bounds__(128)
+#ifndef HJCD_POCCD_MINB
+#define HJCD_POCCD_MINB 4
+#endif
+__global__ void __launch_bounds__(128, HJCD_POCCD_MINB)
 k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float* __restrict__ targets, int T, const float* __restrict__ seeds,
         float* __restrict__ theta_out, float* __restrict__ cost_out, float* __restrict__ ep_out,
@@ -112,19 +115,23 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         }
         if (k == c.ccd_iters) break;
 
-        // Eq. 10 (R2): phi = 2 atan2(|v|, w), a = v / |v|
+        // Eq. 10 (R2): phi = 2 atan2(|v|, w), a = v / |v|; sgn(a . z_j) = sgn(v . z_j)
         const float phi = eo;
-        const float inv_sv = sv > 0.f ? 1.f / sv : 0.f;
-        const float3 ahat = f3(qr.x * inv_sv, qr.y * inv_sv, qr.z * inv_sv);
+        const float3 vq = f3(qr.x, qr.y, qr.z);
         const float dphi = phi > 0.f ? fmaxf(c.delta_min, c.delta0 * rho_k) * phi : 0.f;   // delta(k) phi
         const float tau2 = c.tau_deg * c.tau_deg;
+        // K2b: for an unclamped orientation candidate d = sgn(v.z) dphi,
+        //   |v'|^2 = C^2 |v|^2 + S^2 (w^2 + |v|^2 - (v.z)^2) - 2 C S w |v.z|,
+        // C, S = cos, sin(dphi / 2) shared by all joints (expand q_err (x) q(z, -d))
+        float Cd, Sd;
+        __sincosf(0.5f * dphi, &Sd, &Cd);
+        const float ob0 = Cd * Cd * (sv * sv) + Sd * Sd * (qr.w * qr.w + sv * sv);
+        const float ob1 = Sd * Sd, ob2 = 2.f * Cd * Sd * qr.w;
 
         // ---- Alg. 3 l.6-9: per-joint candidates, scored, greedy argmin
         float best_p = CUDART_INF_F, best_o = CUDART_INF_F;
         int jp = 0, jo = 0;
         float dp_best = 0.f, do_best = 0.f;
-        float3 Pp = f3(0.f, 0.f, 0.f), Zp = f3(0.f, 0.f, 1.f), Po = Pp, Zo = Zp;
-        int typ_p = HJCD_REVOLUTE;
 #pragma unroll
         for (int j = 0; j < NMAX; ++j) {
             if (EXACT || j < n) {
@@ -152,14 +159,21 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
                     const float3 r2 = rp + omc * up - sn * zxu;
                     sp = dot3(r2, r2);
                     // Eq. 11 (R5): delta(k) sgn(a . z_j) phi, sgn(0) = 0
-                    const float az = dot3(ahat, z);
-                    const float sg = az > 0.f ? 1.f : (az < 0.f ? -1.f : 0.f);
-                    dor = clampf(th[j] + sg * dphi, J.lo, J.hi) - th[j];
+                    const float vz = dot3(vq, z);
+                    const float sg = vz > 0.f ? 1.f : (vz < 0.f ? -1.f : 0.f);
+                    const float tsum = th[j] + sg * dphi;
+                    dor = clampf(tsum, J.lo, J.hi) - th[j];
                     // score (K2): |v'|^2 of q_err (x) q(z, -d), monotone in |omega'|
-                    __sincosf(0.5f * dor, &s2, &c2);
-                    if (dor == 0.f) { s2 = 0.f; c2 = 1.f; }
-                    const Quat q2 = qerr_rotate(qr, z, c2, s2);
-                    so = q2.x * q2.x + q2.y * q2.y + q2.z * q2.z;
+                    if (dor == 0.f) {
+                        so = sv * sv;                     // zero step: the current residual, exactly
+                    } else if (tsum >= J.lo && tsum <= J.hi) {
+                        const float avz = fabsf(vz);
+                        so = ob0 - avz * fmaf(ob1, avz, ob2);   // K2b closed form
+                    } else {                              // clamped step: rotate by the effective d
+                        __sincosf(0.5f * dor, &s2, &c2);
+                        const Quat q2 = qerr_rotate(qr, z, c2, s2);
+                        so = q2.x * q2.x + q2.y * q2.y + q2.z * q2.z;
+                    }
                 } else {
                     // prismatic (R32): exact 1-D minimiser z . (P_t - P_ee)
                     dp = clampf(th[j] + dot3(z, rp), J.lo, J.hi) - th[j];
@@ -168,25 +182,32 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
                     dor = 0.f;
                     so = sv * sv;
                 }
-                if (sp < best_p) { best_p = sp; jp = j; dp_best = dp; Pp = P[j]; Zp = z; typ_p = J.type; }
-                if (so < best_o) { best_o = so; jo = j; do_best = dor; Po = P[j]; Zo = z; }
+                if (sp < best_p) { best_p = sp; jp = j; dp_best = dp; }
+                if (so < best_o) { best_o = so; jo = j; do_best = dor; }
             }
         }
 
         // ---- Alg. 3 l.10 + P:201: same joint -> the larger |step|, tie -> position (R8)
-        int ja = -1, jb = -1;      // ja upstream (smaller index), jb downstream
-        float da = 0.f, db = 0.f;
-        float3 Pa = Pp, Za = Zp, Pb = Pp, Zb = Zp;
-        int ta = typ_p, tb = typ_p;
+        int ja = -1, jb;           // ja upstream (smaller index), jb downstream
+        float da = 0.f, db;
         if (jp == jo) {
-            if (fabsf(dp_best) >= fabsf(do_best)) { jb = jp; db = dp_best; }
-            else { jb = jo; db = do_best; Pb = Po; Zb = Zo; tb = HJCD_REVOLUTE; }
+            jb = jp;
+            db = fabsf(dp_best) >= fabsf(do_best) ? dp_best : do_best;
         } else if (jp < jo) {
-            ja = jp; da = dp_best; Pa = Pp; Za = Zp; ta = typ_p;
-            jb = jo; db = do_best; Pb = Po; Zb = Zo; tb = HJCD_REVOLUTE;
+            ja = jp; da = dp_best; jb = jo; db = do_best;
         } else {
-            ja = jo; da = do_best; Pa = Po; Za = Zo; ta = HJCD_REVOLUTE;
-            jb = jp; db = dp_best; Pb = Pp; Zb = Zp; tb = typ_p;
+            ja = jo; da = do_best; jb = jp; db = dp_best;
+        }
+        // frames of the two moved joints (uniform-index selects, no local memory);
+        // an orientation winner is always revolute (prismatic candidates are 0)
+        float3 Pa = f3(0.f, 0.f, 0.f), Za = Pa, Pb = Pa, Zb = Pa;
+        int ta = HJCD_REVOLUTE, tb = HJCD_REVOLUTE;
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) {
+            if (EXACT || j < n) {
+                if (j == ja) { Pa = P[j]; Za = Z[j]; ta = rb.j[j].type; }
+                if (j == jb) { Pb = P[j]; Zb = Z[j]; tb = rb.j[j].type; }
+            }
         }
         // r(theta_hat) exactly: downstream joint's rigid motion first, then the
         // upstream one, both about the pre-update frames (K3)
@@ -230,7 +251,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
                 }
             }
         } else {
-            perturb<NMAX, EXACT>(rb, c, th, c.sigma_ccd, tid, (uint32_t)m, P_PERTURB, (uint32_t)k);   // R11
+            perturb<NMAX, EXACT, true>(rb, c, th, c.sigma_ccd, tid, (uint32_t)m, P_PERTURB, (uint32_t)k);   // R11 (K5)
         }
     }
 

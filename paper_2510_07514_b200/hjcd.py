@@ -15,7 +15,7 @@ from typing import Optional, Tuple
 from . import inputs as _inputs
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhjcd.so")
+LIB_PATH = os.environ.get("HJCD_LIB", os.path.join(_HERE, "libhjcd.so"))   # override: A/B builds
 MAX_DOF = 32
 
 STATUS = {0: "ok", 1: "invalid argument", 2: "unsupported", 3: "CUDA error", 4: "workspace", 5: "nomem"}
