@@ -53,16 +53,6 @@ size_t coop_smem_bytes(int nt) {
     return (size_t)nt * (8 + 4 * (4 * NMAX + 6 + 2) + 4 * 2);
 }
 
-// cascade item q of a seed with flags f -> (direction kind, alpha index)
-__device__ __forceinline__ void decode_item(int q, int f, int A, int& kind, int& a) {
-    const int nlm = (f & 1) ? A : 0;
-    const int ndl = (f & 2) ? 1 : 0;
-    if (q < nlm) { kind = 0; a = q + 1; return; }
-    q -= nlm;
-    if (q < ndl) { kind = 1; a = 0; return; }
-    kind = 2;
-    a = q - ndl;
-}
 
 template <int NMAX, bool EXACT>
 __global__ void __launch_bounds__(256)

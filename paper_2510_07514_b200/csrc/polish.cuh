@@ -232,4 +232,15 @@ __device__ __forceinline__ bool single_coord_direction(const DevRobot& rb, const
     return true;
 }
 
+// cascade item q of a seed with flags f -> (direction kind, alpha index)
+__device__ __forceinline__ void decode_item(int q, int f, int A, int& kind, int& a) {
+    const int nlm = (f & 1) ? A : 0;
+    const int ndl = (f & 2) ? 1 : 0;
+    if (q < nlm) { kind = 0; a = q + 1; return; }
+    q -= nlm;
+    if (q < ndl) { kind = 1; a = 0; return; }
+    kind = 2;
+    a = q - ndl;
+}
+
 }  // namespace hjcd
