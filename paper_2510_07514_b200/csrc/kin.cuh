@@ -61,37 +61,29 @@ __device__ __forceinline__ Quat qerr_rotate(Quat q, float3 z, float c2, float s2
     return r;
 }
 
-// rotation matrix (row-major) -> unit quaternion, w >= 0 (Shepperd).  With
-// t the pivot (>= 1/4 in the chosen branch), s = 2 sqrt(t) and 1/s =
-// rsqrt(t)/2, so no division is needed.
+// rotation matrix (row-major) -> unit quaternion, w >= 0 (Shepperd), without
+// branches: the four pivots 4q_i^2 = t_i are formed, the largest is chosen by
+// selects, and q = (column of the symmetric 4x4 form) * rsqrt(t)/2.  Seeds of
+// a warp sit in different quadrants, so the branchy form diverges 4 ways.
 __device__ __forceinline__ Quat quat_from_rot(const float R[9]) {
-    float tr = R[0] + R[4] + R[8];
+    const float t0 = 1.f + R[0] + R[4] + R[8];   // 4 w^2
+    const float t1 = 1.f + R[0] - R[4] - R[8];   // 4 x^2
+    const float t2 = 1.f - R[0] + R[4] - R[8];   // 4 y^2
+    const float t3 = 1.f - R[0] - R[4] + R[8];   // 4 z^2
+    const float a = R[7] - R[5], b = R[2] - R[6], cc = R[3] - R[1];   // 4wx, 4wy, 4wz
+    const float d = R[1] + R[3], e = R[2] + R[6], f = R[5] + R[7];    // 4xy, 4xz, 4yz
+    // same branch order as the classic form: w if tr > 0, else the largest diagonal
+    const bool pw = (R[0] + R[4] + R[8]) > 0.f;
+    const bool px = !pw && R[0] > R[4] && R[0] > R[8];
+    const bool py = !pw && !px && R[4] > R[8];
+    float t, qw, qx, qy, qz;   // the pivot's column, scaled by 4 q_pivot
+    if (pw) { t = t0; qw = t0; qx = a; qy = b; qz = cc; }
+    else if (px) { t = t1; qw = a; qx = t1; qy = d; qz = e; }
+    else if (py) { t = t2; qw = b; qx = d; qy = t2; qz = f; }
+    else { t = t3; qw = cc; qx = e; qy = f; qz = t3; }
+    const float is = 0.5f * rsqrtf(t);
     Quat q;
-    if (tr > 0.f) {
-        const float t = tr + 1.f, r = rsqrtf(t), is = 0.5f * r;
-        q.w = 0.5f * t * r;
-        q.x = (R[7] - R[5]) * is;
-        q.y = (R[2] - R[6]) * is;
-        q.z = (R[3] - R[1]) * is;
-    } else if (R[0] > R[4] && R[0] > R[8]) {
-        const float t = 1.f + R[0] - R[4] - R[8], r = rsqrtf(t), is = 0.5f * r;
-        q.w = (R[7] - R[5]) * is;
-        q.x = 0.5f * t * r;
-        q.y = (R[1] + R[3]) * is;
-        q.z = (R[2] + R[6]) * is;
-    } else if (R[4] > R[8]) {
-        const float t = 1.f + R[4] - R[0] - R[8], r = rsqrtf(t), is = 0.5f * r;
-        q.w = (R[2] - R[6]) * is;
-        q.x = (R[1] + R[3]) * is;
-        q.y = 0.5f * t * r;
-        q.z = (R[5] + R[7]) * is;
-    } else {
-        const float t = 1.f + R[8] - R[0] - R[4], r = rsqrtf(t), is = 0.5f * r;
-        q.w = (R[3] - R[1]) * is;
-        q.x = (R[2] + R[6]) * is;
-        q.y = (R[5] + R[7]) * is;
-        q.z = 0.5f * t * r;
-    }
+    q.w = qw * is; q.x = qx * is; q.y = qy * is; q.z = qz * is;
     // renormalise (absorbs the rsqrt approximation and FK rounding)
     float inv = rsqrtf(q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z);
     if (q.w < 0.f) inv = -inv;
