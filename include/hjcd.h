@@ -181,6 +181,17 @@ hjcd_status hjcd_poccd(const hjcd_robot* r, const hjcd_config* c, const float* t
                        const float* seeds, float* theta, float* cost, float* pos_err,
                        float* ori_err, int32_t* iters, hjcd_stream_t stream);
 
+/* Classic position-only CCD (Alg. 1), the baseline PO-CCD extends
+ * (ablation): T targets x c->M seeds, joints swept tip to root,
+ * signed projected-angle steps (Eqs. 8-9; R3, R4) clamped to the limits (R7);
+ * a seed stops when |P_ee - P_t| < c->eps_p_coarse (Alg. 1 l.7, R12) or after
+ * c->ccd_iters sweeps.  Orientation is ignored (position-only IK).
+ *   seeds [T][dof][M] or NULL (the PO-CCD Philox seeds, R30);
+ *   theta [T][dof][M] out; pos_err [T][M] out or NULL; iters [T][M] out or NULL. */
+hjcd_status hjcd_ccd(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                     const float* seeds, float* theta, float* pos_err, int32_t* iters,
+                     hjcd_stream_t stream);
+
 /* Top-K by (cost, seed index) + floor(B/K) replicas (Alg. 2 l.2-8; R14, R15).
  *   cost [T][M], theta [T][dof][M] in; polish_seeds [T][B][dof] out (slot
  *   b = copy*K + rank; slots >= floor(B/K)*K are NaN); kept_idx [T][K] out or NULL.

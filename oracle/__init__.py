@@ -75,6 +75,7 @@ def lib():
         _lib.oracle_uniform_seeds.argtypes = [P, u64, i64, i32, P]
         _lib.oracle_fk.argtypes = [P, P, i32, P, P, P, P]
         _lib.oracle_po_ccd.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P]
+        _lib.oracle_ccd.argtypes = [P, P, P, i32, i64, P, P, P, P]
         _lib.oracle_select_replicate.argtypes = [P, P, P, P, i32, i64, P, P]
         _lib.oracle_pj_ik.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P]
         _lib.oracle_solve.argtypes = [P, P, P, i32, i64, P, P, P, P]
@@ -255,6 +256,18 @@ def po_ccd(chain, params, targets, tid_offset: int = 0, seeds: Optional[np.ndarr
     lib().oracle_po_ccd(_ref(r), _ref(c), _p(tg), T, tid_offset, _p(sd), _p(out["theta"]),
                         _p(out["cost"]), _p(out["ep"]), _p(out["eo"]), _p(out["iters"]),
                         _p(out["margin"]))
+    return out
+
+
+def ccd(chain, params, targets, tid_offset: int = 0, seeds: Optional[np.ndarray] = None):
+    """Classic CCD (Alg. 1) for T x M seeds -> dict theta [T,n,M], ep, iters [T,M]."""
+    r, c = make_robot(chain), make_config(params)
+    tg = np.ascontiguousarray(targets, dtype=np.float32).reshape(-1, 7)
+    T, n, M = tg.shape[0], chain.dof, params["M"]
+    sd = None if seeds is None else np.ascontiguousarray(seeds, dtype=np.float64)
+    out = dict(theta=np.empty((T, n, M)), ep=np.empty((T, M)), iters=np.empty((T, M), dtype=np.int32))
+    lib().oracle_ccd(_ref(r), _ref(c), _p(tg), T, tid_offset, _p(sd), _p(out["theta"]), _p(out["ep"]),
+                     _p(out["iters"]))
     return out
 
 

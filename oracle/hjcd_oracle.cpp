@@ -583,6 +583,35 @@ void po_ccd_target(const Robot& rb, const OracleConfig& c, const Target& tgt, ui
     }
 }
 
+/* ---------------- classic CCD, one seed (Alg. 1) ----------------
+ * Literal: joints j = n..1 (tip to root); for each, a FULL FK at the current
+ * theta, Eqs. 8-9 (R3 sign, R4 degeneracy), clamp to the limits (R7), update;
+ * after the sweep an FK and the test |P_ee - P_t| < eps (R12's unsquared
+ * reading of Alg. 1 l.7, eps = eps_p_coarse), checked before each sweep. */
+SeedOut ccd_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, std::vector<double>& th) {
+    const OracleRobot* r = rb.r;
+    int n = rb.dof;
+    SeedOut so = {INF, INF, 0, INF};
+    Frames F;
+    int k;
+    for (k = 0;; ++k) {
+        fk(rb, th.data(), F);
+        so.ep = norm(sub(tgt.p, F.pee));
+        if (so.ep < c.eps_p_coarse) break;
+        if (k == c.ccd_iters) break;
+        for (int j = n - 1; j >= 0; --j) {
+            fk(rb, th.data(), F);                 /* literal: FK at the current theta */
+            int ent = rb.dof_entry[j];
+            double step;
+            if (r->type[ent] == 0) step = ccd_position_step(F.P[j], F.z[j], F.pee, tgt.p, c.tau_deg, nullptr);
+            else step = dot(F.z[j], sub(tgt.p, F.pee));
+            th[j] = clampd(th[j] + step, r->lo[ent], r->hi[ent]);
+        }
+    }
+    so.iters = k;
+    return so;
+}
+
 /* uniform seed in limits (Alg. 3 l.2-3), fp32 fmaf on purpose (R30) */
 void uniform_seed(const Robot& rb, uint64_t seed, uint64_t tid, uint32_t sid, double* th) {
     for (int j = 0; j < rb.dof; ++j) {
@@ -1094,6 +1123,29 @@ void oracle_po_ccd(const OracleRobot* r, const OracleConfig* c, const float* tar
             seed_of(t, m, tid, th);
             SeedOut so = po_ccd_seed(rb, *c, tgt, tid, (uint32_t)m, th);
             emit(t, m, th, so);
+        }
+    }
+}
+
+/* classic CCD (Alg. 1) for T targets x M seeds: seeds f64 [T][n][M] or NULL
+ * (Philox uniform, as PO-CCD); out theta f64 [T][n][M], ep f64 [T][M], iters i32 [T][M] */
+void oracle_ccd(const OracleRobot* r, const OracleConfig* c, const float* targets, int32_t T,
+                int64_t tid_offset, const double* seeds, double* theta, double* ep, int32_t* iters) {
+    Robot rb = make_robot(r);
+    int n = rb.dof, M = c->M;
+#pragma omp parallel for collapse(2) schedule(dynamic, 4)
+    for (int t = 0; t < T; ++t) {
+        for (int m = 0; m < M; ++m) {
+            Target tgt = read_target(targets + (size_t)t * 7);
+            uint64_t tid = (uint64_t)(tid_offset + t);
+            std::vector<double> th(n);
+            if (seeds) for (int j = 0; j < n; ++j) th[j] = seeds[((size_t)t * n + j) * M + m];
+            else uniform_seed(rb, c->rng_seed, tid, (uint32_t)m, th.data());
+            SeedOut so = ccd_seed(rb, *c, tgt, th);
+            for (int j = 0; j < n; ++j) theta[((size_t)t * n + j) * M + m] = th[j];
+            size_t o = (size_t)t * M + m;
+            if (ep) ep[o] = so.ep;
+            if (iters) iters[o] = so.iters;
         }
     }
 }

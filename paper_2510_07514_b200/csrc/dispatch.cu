@@ -42,4 +42,12 @@ cudaError_t launch_pjik(const DevRobot& rb, const DevCfg& c, const float* target
     return launch_pjik_coop(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
 }
 
+cudaError_t launch_ccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* seeds,
+                       float* theta, float* ep, int32_t* iters, cudaStream_t s) {
+    if (rb.n == 7) return launch_ccd_t<7, true>(rb, c, targets, T, seeds, theta, ep, iters, s);
+    if (rb.n <= 8) return launch_ccd_t<8, false>(rb, c, targets, T, seeds, theta, ep, iters, s);
+    if (rb.n <= 16) return launch_ccd_t<16, false>(rb, c, targets, T, seeds, theta, ep, iters, s);
+    return launch_ccd_t<32, false>(rb, c, targets, T, seeds, theta, ep, iters, s);
+}
+
 }  // namespace hjcd

@@ -394,6 +394,16 @@ hjcd_status hjcd_poccd(const hjcd_robot* r, const hjcd_config* c, const float* t
     return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
 }
 
+hjcd_status hjcd_ccd(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T, const float* seeds,
+                     float* theta, float* pos_err, int32_t* iters, hjcd_stream_t stream) {
+    if (!r || !c || !targets || T < 1 || !theta) return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    cudaError_t e = launch_ccd(r->dev, d, targets, T, seeds, theta, pos_err, iters, (cudaStream_t)stream);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+}
+
 hjcd_status hjcd_select_replicate(const hjcd_robot* r, const hjcd_config* c, const float* cost,
                                   const float* theta, int32_t T, float* polish_seeds, int32_t* kept_idx,
                                   hjcd_stream_t stream) {

@@ -54,6 +54,9 @@ cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* tar
                            const float* seeds, float* theta, float* cost, float* ep, float* eo,
                            int32_t* iters, cudaStream_t s);
 template <int NMAX, bool EXACT>
+cudaError_t launch_ccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* seeds,
+                         float* theta, float* ep, int32_t* iters, cudaStream_t s);
+template <int NMAX, bool EXACT>
 cudaError_t launch_coop_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                           const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
                           int32_t* iters, cudaStream_t s);
@@ -64,6 +67,8 @@ cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, f
 cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                          const float* seeds, float* theta, float* cost, float* ep, float* eo,
                          int32_t* iters, cudaStream_t s);
+cudaError_t launch_ccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* seeds,
+                       float* theta, float* ep, int32_t* iters, cudaStream_t s);
 cudaError_t launch_select_replicate(const DevRobot& rb, const DevCfg& c, const float* cost,
                                     const float* theta, int T, float* seeds, int32_t* kept,
                                     cudaStream_t s);

@@ -24,7 +24,7 @@ TARGET_CONVERGED, TARGET_SUCCESS, TARGET_NOT_CONVERGED, TARGET_INVALID = 0, 1, 2
 EXPORTS = [
     "hjcd_robot_create", "hjcd_robot_extend", "hjcd_robot_destroy", "hjcd_robot_dof",
     "hjcd_robot_limits", "hjcd_config_default", "hjcd_workspace_size",
-    "hjcd_workspace_size_host", "hjcd_solve", "hjcd_solve_timed", "hjcd_solve_host", "hjcd_fk", "hjcd_poccd",
+    "hjcd_workspace_size_host", "hjcd_solve", "hjcd_solve_timed", "hjcd_solve_host", "hjcd_ccd", "hjcd_fk", "hjcd_poccd",
     "hjcd_select_replicate", "hjcd_pjik", "hjcd_select_best", "hjcd_status_string",
     "hjcd_last_cuda_error", "hjcd_version",
 ]
@@ -81,6 +81,7 @@ def lib():
         L.hjcd_solve_host.argtypes = [P, P, P, i32, P, P, P, P, P, sz, P]
         L.hjcd_fk.argtypes = [P, P, i32, P, P, P]
         L.hjcd_poccd.argtypes = [P, P, P, i32, P, P, P, P, P, P, P]
+        L.hjcd_ccd.argtypes = [P, P, P, i32, P, P, P, P, P]
         L.hjcd_select_replicate.argtypes = [P, P, P, P, i32, P, P, P]
         L.hjcd_pjik.argtypes = [P, P, P, i32, P, P, P, P, P, P, P]
         L.hjcd_select_best.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P]
@@ -315,6 +316,22 @@ def poccd(robot: Robot, cfg: hjcd_config, targets, seeds=None, stream=None):
     _check(lib().hjcd_poccd(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(seeds),
                             _ptr(out["theta"]), _ptr(out["cost"]), _ptr(out["ep"]),
                             _ptr(out["eo"]), _ptr(out["iters"]), _stream(stream)), "hjcd_poccd")
+    return out
+
+
+def ccd(robot: Robot, cfg: hjcd_config, targets, seeds=None, stream=None):
+    """Classic position-only CCD (Alg. 1): -> dict theta [T, n, M], ep [T, M], iters [T, M]."""
+    torch = _torch()
+    T, n, M = targets.shape[0], robot.dof, cfg.M
+    _dev_f32(targets, (T, 7), "targets")
+    if seeds is not None:
+        _dev_f32(seeds, (T, n, M), "seeds")
+    d = targets.device
+    out = dict(theta=torch.empty((T, n, M), dtype=torch.float32, device=d),
+               ep=torch.empty((T, M), dtype=torch.float32, device=d),
+               iters=torch.empty((T, M), dtype=torch.int32, device=d))
+    _check(lib().hjcd_ccd(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(seeds), _ptr(out["theta"]),
+                          _ptr(out["ep"]), _ptr(out["iters"]), _stream(stream)), "hjcd_ccd")
     return out
 
 

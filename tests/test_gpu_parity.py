@@ -163,6 +163,32 @@ def test_poccd_lockstep_is_truncated_per_seed_run(hjcd_lib, cuda, name, M):
         assert (d < 1e-4).mean() >= 0.97, (t, (d < 1e-4).mean())
 
 
+@pytest.mark.parametrize("name,iters,floor", [("panda", 4, 0.9), ("panda", 32, 0.6), ("fetch", 8, 0.8),
+                                              ("planar2", 64, 0.8)])
+def test_ccd_parity(hjcd_lib, cuda, name, iters, floor):
+    # classic CCD (Alg. 1, f4 ablation): per seed after a fixed number of sweeps
+    ch = inputs.planar([0.6, 0.4]) if name == "planar2" else inputs.robot(name)
+    rb = hjcd_lib.Robot(ch)
+    p = params(M=257, ccd_iters=iters)
+    tg, _ = targets_for(ch, 3)
+    out = hjcd_lib.ccd(rb, hjcd_lib.config_from_params(p), T(tg, cuda))
+    ref = oracle.ccd(ch, p, tg)
+    ep = N(out["ep"])
+    agree = np.abs(ep - ref["ep"]) <= TOL_P
+    assert agree.mean() >= floor, agree.mean()
+    th = N(out["theta"]).astype(np.float64)
+    lo, hi = [x.astype(np.float32).astype(np.float64) for x in ch.limits()]
+    assert np.all(th >= lo[None, :, None]) and np.all(th <= hi[None, :, None])
+    # reported errors are those of the returned theta
+    Tn, n, M = th.shape
+    pose = oracle.fk(ch, th.transpose(0, 2, 1).reshape(-1, n)).reshape(Tn, M, 7)
+    ep64 = np.linalg.norm(pose[..., :3] - tg[:, None, :3].astype(np.float64), axis=-1)
+    assert np.abs(ep64 - ep).max() < 2e-6
+    # converged seeds stop with the same iteration count on both sides
+    both = (N(out["iters"]) < iters) & (ref["iters"] < iters) & agree
+    assert np.all(np.abs(N(out["iters"])[both] - ref["iters"][both]) <= 1)
+
+
 def test_poccd_seeded_on_answer(hjcd_lib, cuda):
     # target = FK(seed 0) -> converged at iteration 0
     ch = inputs.panda()
@@ -362,6 +388,28 @@ def test_full_size_c2(hjcd_lib, cuda):
     qh, peh, oeh, sth = hjcd_lib.solve_host(rb, tg, cfg)
     assert np.array_equal(qh.numpy(), q) and np.array_equal(sth.numpy(), st)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("name,Tn", [("fetch", 10000), ("panda_x14", 10000)])
+def test_full_size_c3_c4(hjcd_lib, cuda, name, Tn):
+    """BASELINE configs[2]/[3] at bench.py's launch size (10,000 targets x M=1000,
+    defaults): two sampled targets against the oracle (own global ids);
+    properties over all targets."""
+    ch = inputs.robot(name)
+    rb = hjcd_lib.Robot(ch)
+    tg, _ = targets_for(ch, Tn)
+    p = params()
+    cfg = hjcd_lib.config_from_params(p)
+    q, pe, oe, st = [N(x) for x in hjcd_lib.solve(rb, T(tg, cuda), cfg)]
+    pe64, oe64 = fp64_errors(ch, q, tg)
+    assert np.abs(pe64 - pe).max() < 2e-6 and np.abs(oe64 - oe).max() < 2e-5
+    assert success(pe64, oe64).mean() >= 0.99
+    lo, hi = [x.astype(np.float32) for x in ch.limits()]
+    assert np.all(q >= lo) and np.all(q <= hi)
+    assert np.all((st <= 1) == success(pe64, oe64)) or abs(np.mean(st <= 1) - success(pe64, oe64).mean()) < 1e-3
+    for i in (17, Tn - 1):
+        rq, rpe, roe, rst = oracle.solve(ch, p, tg[i:i + 1], tid_offset=i)
+        assert success(rpe, roe)[0] == success(pe64[i:i + 1], oe64[i:i + 1])[0]
 
 
 def test_edge_cases(hjcd_lib, cuda):

@@ -470,6 +470,69 @@ def test_poccd_target_early_exit_is_lockstep_truncation():
                 assert np.any((ex["ep"][t] < 5e-3) & (ex["eo"][t] < 5e-2))
 
 
+# ---------------------------------------------------------------- classic CCD (Alg. 1)
+def _planar_fk(L1, L2, th):
+    x1 = np.array([L1 * math.cos(th[0]), L1 * math.sin(th[0])])
+    return x1, x1 + L2 * np.array([math.cos(th[0] + th[1]), math.sin(th[0] + th[1])])
+
+
+def test_ccd_one_sweep_planar_by_hand():
+    # Alg. 1 on a planar 2-link arm (z axes): one sweep = rotate the tip joint so
+    # its link points at the target, then the base joint so the (moved) end
+    # effector points at the target; angles from plane geometry (atan2 of the
+    # joint-to-point vectors), wrapped to (-pi, pi]
+    L1, L2 = 0.6, 0.4
+    ch = inputs.planar([L1, L2], lo=-math.pi, hi=math.pi)
+    th0 = np.array([0.3, -0.4])
+    pt = np.array([0.2, 0.7])
+    tg = oracle.fk(ch, np.array([[1.1, 0.9]])).astype(np.float32)
+    tg[0, :2] = pt
+    tg[0, 2] = 0.0
+    p = params(M=1, ccd_iters=1, eps_p_coarse=1e-12)
+    r = oracle.ccd(ch, p, tg, seeds=th0.reshape(1, 2, 1))
+    wrap = lambda a: (a + math.pi) % (2 * math.pi) - math.pi
+    th = th0.copy()
+    p1, pe = _planar_fk(L1, L2, th)
+    th[1] += wrap(math.atan2(*(pt - p1)[::-1]) - math.atan2(*(pe - p1)[::-1]))
+    p1, pe = _planar_fk(L1, L2, th)
+    th[0] += wrap(math.atan2(pt[1], pt[0]) - math.atan2(pe[1], pe[0]))
+    tg64 = tg.astype(np.float64)[0, :2]
+    assert np.allclose(tg64, pt, atol=1e-7)
+    assert np.abs(r["theta"][0, :, 0] - th).max() < 1e-6, (r["theta"][0, :, 0], th)
+
+
+def test_ccd_converges_to_closed_form_planar_ik():
+    # position-only 2-link planar IK has exactly two solutions (elbow up/down):
+    # cos q2 = (|p|^2 - L1^2 - L2^2) / (2 L1 L2), q1 = atan2(p) - atan2(L2 s2, L1 + L2 c2)
+    L1, L2 = 0.6, 0.4
+    ch = inputs.planar([L1, L2], lo=-math.pi, hi=math.pi)
+    tg = oracle.fk(ch, np.array([[0.7, -1.1]])).astype(np.float32)
+    pt = tg[0, :2].astype(np.float64)
+    c2 = (pt @ pt - L1 ** 2 - L2 ** 2) / (2 * L1 * L2)
+    sols = []
+    for s2 in (math.sqrt(1 - c2 * c2), -math.sqrt(1 - c2 * c2)):
+        q2 = math.atan2(s2, c2)
+        q1 = math.atan2(pt[1], pt[0]) - math.atan2(L2 * s2, L1 + L2 * c2)
+        sols.append(np.array([q1, q2]))
+    # the literal arccos of Eq. 9 cannot resolve steps below ~1.5e-8 rad in
+    # fp64 (acos(1 - 2^-53)), so "converged" means |P_ee - P_t| < 1e-7 m here;
+    # seeds that hit a +-pi limit may stall elsewhere (CCD is a local method)
+    p = params(M=16, ccd_iters=400, eps_p_coarse=1e-7)
+    r = oracle.ccd(ch, p, tg)
+    wrap = lambda a: (a + math.pi) % (2 * math.pi) - math.pi
+    ok = 0
+    for m in range(16):
+        th = r["theta"][0, :, m]
+        if r["ep"][0, m] < 1e-7:
+            d = min(np.abs(wrap(th - s)).max() for s in sols)
+            assert d < 1e-6, (th, sols)
+            ok += 1
+    assert ok >= 6, r["ep"]
+    # the error never exceeds the seed's (CCD steps are 1-D minimisers)
+    r0 = oracle.ccd(ch, params(M=16, ccd_iters=0), tg)
+    assert np.all(r["ep"] <= r0["ep"] + 1e-12)
+
+
 # ---------------------------------------------------------------- P15 PJ-IK special cases
 def test_pjik_zero_error_fixed_point_and_convergence():
     ch = inputs.panda()
