@@ -157,6 +157,17 @@ hjcd_status hjcd_solve_timed(const hjcd_robot* r, const hjcd_config* c, const fl
                              void* workspace, size_t workspace_bytes, hjcd_stream_t stream,
                              void* const* events);
 
+/* The solution BATCH ("the return of multiple local optima"; §V-C
+ * keeps "the best 50 joint configurations"): Alg. 2 with the final
+ * best-select replaced by the best N <= floor(B/K)*K polished seeds of each
+ * target, in R27 order (fine-converged first, then the cost c of R14, then
+ * slot), so entry 0 is hjcd_solve's answer.
+ *   q_out [T][N][dof], pos_err/ori_err [T][N] device out; status [T] of entry 0.
+ *   workspace as hjcd_solve. */
+hjcd_status hjcd_solve_batch(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                             int32_t N, float* q_out, float* pos_err, float* ori_err, int32_t* status,
+                             void* workspace, size_t workspace_bytes, hjcd_stream_t stream);
+
 /* The same with HOST buffers (same shapes): copies targets host->device,
  * solves, copies results device->host, and synchronises `stream` before
  * returning.  workspace: device, >= hjcd_workspace_size_host bytes. */
@@ -215,6 +226,24 @@ hjcd_status hjcd_select_best(const hjcd_robot* r, const hjcd_config* c, const fl
                              int32_t T, const float* theta, const float* pos_err_all,
                              const float* ori_err_all, float* q_out, float* pos_err,
                              float* ori_err, int32_t* status, hjcd_stream_t stream);
+
+/* Best N of the B polished seeds per target (the stage of hjcd_solve_batch):
+ * theta [T][B][dof], pos_err_all/ori_err_all [T][B] in; q_out [T][N][dof],
+ * pos_err/ori_err [T][N], idx [T][N] (slot, or -1 for an invalid target; may be
+ * NULL) out.  1 <= N <= floor(B/K)*K. */
+hjcd_status hjcd_select_topn(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                             const float* theta, const float* pos_err_all, const float* ori_err_all,
+                             int32_t N, float* q_out, float* pos_err, float* ori_err, int32_t* idx,
+                             hjcd_stream_t stream);
+
+/* Solution-set diversity (§V-C, Table III; R36): for each of T pairs
+ * of point sets X [T][N][dim], Y [T][N2][dim] (device, fp32), the biased
+ * V-statistic MMD^2 = mean k(x,x') + mean k(y,y') - 2 mean k(x,y) with the
+ * Gaussian kernel k(a,b) = exp(-|a-b|^2 / (2 h^2)), h = median of the pairwise
+ * distances over X u Y (h is written to bandwidth [T] if non-NULL).
+ * N, N2 >= 1, N + N2 <= 256 (E_UNSUPPORTED), 1 <= dim <= 32.  MMD = sqrt(max(0, MMD^2)). */
+hjcd_status hjcd_mmd(const float* X, int32_t N, const float* Y, int32_t N2, int32_t dim, int32_t T,
+                     float* mmd2, float* bandwidth, hjcd_stream_t stream);
 
 const char* hjcd_status_string(hjcd_status s);
 /* text of the last CUDA error seen by this thread's calls ("" if none) */

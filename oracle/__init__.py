@@ -11,6 +11,7 @@ Every function cites the PAPER.md passage it follows; see hjcd_oracle.cpp.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 from typing import Dict, Optional
@@ -311,6 +312,48 @@ def solve(chain, params, targets, tid_offset: int = 0):
     st = np.empty(T, dtype=np.int32)
     lib().oracle_solve(_ref(r), _ref(c), _p(tg), T, tid_offset, _p(q), _p(pe), _p(oe), _p(st))
     return q, pe, oe, st
+
+
+def select_topn(params, ep, eo, N: int):
+    """Best N of the B polished seeds per target in R27 order (fine-converged
+    first, then c = w_p^2 ep^2 + w_o^2 eo^2 (R14), then slot): a stable sort on
+    the (tier, cost) key.  ep, eo [T, B] -> idx [T, N]."""
+    used = (params["B"] // params["K"]) * params["K"]
+    ep = np.asarray(ep, dtype=np.float64)[:, :used]
+    eo = np.asarray(eo, dtype=np.float64)[:, :used]
+    cost = params["w_p"] ** 2 * ep ** 2 + params["w_o"] ** 2 * eo ** 2
+    cost = np.where(cost >= 0, cost, np.inf)
+    tier = ~((ep < params["eps_p_fine"]) & (eo < params["eps_o_fine"]))
+    out = np.empty((ep.shape[0], N), dtype=np.int64)
+    for t in range(ep.shape[0]):
+        order = sorted(range(used), key=lambda b: (bool(tier[t, b]), cost[t, b], b))
+        out[t] = order[:N]
+    return out
+
+
+def mmd2(X, Y):
+    """Maximum mean discrepancy (PAPER §V-C, Table III; R36): biased
+    V-statistic of MMD^2 between point sets X [N, d] and Y [N2, d] with the
+    Gaussian kernel k(a, b) = exp(-|a - b|^2 / (2 h^2)), h = median of the
+    pairwise distances (i < j) over X u Y.  Plain fp64 definition.
+    Returns (MMD^2, h)."""
+    X = np.asarray(X, dtype=np.float64)
+    Y = np.asarray(Y, dtype=np.float64)
+    Z = np.concatenate([X, Y])
+    L = len(Z)
+    d = [np.linalg.norm(Z[i] - Z[j]) for i in range(L) for j in range(i + 1, L)]
+    h = float(np.median(d))
+
+    def k(a, b):
+        s = float(np.sum((a - b) ** 2))
+        if h > 0:
+            return math.exp(-s / (2.0 * h * h))
+        return 1.0 if s == 0.0 else 0.0
+
+    kxx = sum(k(a, b) for a in X for b in X) / (len(X) ** 2)
+    kyy = sum(k(a, b) for a in Y for b in Y) / (len(Y) ** 2)
+    kxy = sum(k(a, b) for a in X for b in Y) / (len(X) * len(Y))
+    return kxx + kyy - 2.0 * kxy, h
 
 
 def num_threads() -> int:

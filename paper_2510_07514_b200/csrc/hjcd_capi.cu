@@ -342,6 +342,58 @@ hjcd_status hjcd_solve_timed(const hjcd_robot* r, const hjcd_config* c, const fl
     return HJCD_OK;
 }
 
+hjcd_status hjcd_solve_batch(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T, int32_t N,
+                             float* q_out, float* pos_err, float* ori_err, int32_t* status, void* workspace,
+                             size_t workspace_bytes, hjcd_stream_t stream) {
+    if (!r || !c || !targets || T < 1 || !q_out || !pos_err || !ori_err || !status || !workspace)
+        return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    if (N < 1 || N > d.copies * d.K) return HJCD_E_INVALID_ARG;
+    if (c->M > 8192) return HJCD_E_UNSUPPORTED;
+    if ((st = check_poccd(c)) != HJCD_OK) return st;
+    Layout L = layout(r->dof, T, c);
+    if (workspace_bytes < L.total || ((uintptr_t)workspace & 255)) return HJCD_E_WORKSPACE;
+    char* ws = (char*)workspace;
+    float* theta1 = (float*)(ws + L.theta1);
+    float* cost1 = (float*)(ws + L.cost1);
+    float* seeds2 = (float*)(ws + L.seeds2);
+    float* ep2 = (float*)(ws + L.ep2);
+    float* eo2 = (float*)(ws + L.eo2);
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    if ((e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s)) != cudaSuccess ||
+        (e = launch_select_replicate(r->dev, d, cost1, theta1, T, seeds2, nullptr, s)) != cudaSuccess ||
+        (e = launch_pjik(r->dev, d, targets, T, seeds2, seeds2, ep2, eo2, nullptr, nullptr, s)) != cudaSuccess ||
+        (e = launch_select_topn(r->dev, d, targets, T, seeds2, ep2, eo2, N, q_out, pos_err, ori_err, nullptr, status,
+                                s)) != cudaSuccess)
+        return cuda_fail(e);
+    return HJCD_OK;
+}
+
+hjcd_status hjcd_select_topn(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                             const float* theta, const float* pos_err_all, const float* ori_err_all, int32_t N,
+                             float* q_out, float* pos_err, float* ori_err, int32_t* idx, hjcd_stream_t stream) {
+    if (!r || !c || !targets || T < 1 || !theta || !pos_err_all || !ori_err_all || !q_out || !pos_err || !ori_err)
+        return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    if (N < 1 || N > d.copies * d.K) return HJCD_E_INVALID_ARG;
+    cudaError_t e = launch_select_topn(r->dev, d, targets, T, theta, pos_err_all, ori_err_all, N, q_out, pos_err,
+                                       ori_err, idx, nullptr, (cudaStream_t)stream);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+}
+
+hjcd_status hjcd_mmd(const float* X, int32_t N, const float* Y, int32_t N2, int32_t dim, int32_t T, float* mmd2,
+                     float* bandwidth, hjcd_stream_t stream) {
+    if (!X || !Y || !mmd2 || N < 1 || N2 < 1 || T < 1 || dim < 1 || dim > HJCD_MAX_DOF) return HJCD_E_INVALID_ARG;
+    if (N + N2 > 256) return HJCD_E_UNSUPPORTED;
+    cudaError_t e = launch_mmd(X, N, Y, N2, dim, T, mmd2, bandwidth, (cudaStream_t)stream);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+}
+
 hjcd_status hjcd_solve_host(const hjcd_robot* r, const hjcd_config* c, const float* targets_host, int32_t T,
                             float* q_host, float* pos_err_host, float* ori_err_host, int32_t* status_host,
                             void* workspace, size_t workspace_bytes, hjcd_stream_t stream) {

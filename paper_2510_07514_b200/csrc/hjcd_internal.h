@@ -78,6 +78,11 @@ cudaError_t launch_pjik(const DevRobot& rb, const DevCfg& c, const float* target
 cudaError_t launch_pjik_coop(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                              const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
                              int32_t* iters, cudaStream_t s);
+cudaError_t launch_select_topn(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* theta,
+                               const float* ep_all, const float* eo_all, int N, float* q_out, float* pos_err,
+                               float* ori_err, int32_t* idx, int32_t* status, cudaStream_t s);
+cudaError_t launch_mmd(const float* X, int N, const float* Y, int N2, int n, int T, float* mmd2, float* bw,
+                       cudaStream_t s);
 cudaError_t launch_select_best(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                const float* theta, const float* ep_all, const float* eo_all,
                                float* q_out, float* pos_err, float* ori_err, int32_t* status,

@@ -24,7 +24,8 @@ TARGET_CONVERGED, TARGET_SUCCESS, TARGET_NOT_CONVERGED, TARGET_INVALID = 0, 1, 2
 EXPORTS = [
     "hjcd_robot_create", "hjcd_robot_extend", "hjcd_robot_destroy", "hjcd_robot_dof",
     "hjcd_robot_limits", "hjcd_config_default", "hjcd_workspace_size",
-    "hjcd_workspace_size_host", "hjcd_solve", "hjcd_solve_timed", "hjcd_solve_host", "hjcd_ccd", "hjcd_fk", "hjcd_poccd",
+    "hjcd_workspace_size_host", "hjcd_solve", "hjcd_solve_timed", "hjcd_solve_host", "hjcd_ccd",
+    "hjcd_solve_batch", "hjcd_select_topn", "hjcd_mmd", "hjcd_fk", "hjcd_poccd",
     "hjcd_select_replicate", "hjcd_pjik", "hjcd_select_best", "hjcd_status_string",
     "hjcd_last_cuda_error", "hjcd_version",
 ]
@@ -82,6 +83,9 @@ def lib():
         L.hjcd_fk.argtypes = [P, P, i32, P, P, P]
         L.hjcd_poccd.argtypes = [P, P, P, i32, P, P, P, P, P, P, P]
         L.hjcd_ccd.argtypes = [P, P, P, i32, P, P, P, P, P]
+        L.hjcd_solve_batch.argtypes = [P, P, P, i32, i32, P, P, P, P, P, sz, P]
+        L.hjcd_select_topn.argtypes = [P, P, P, i32, P, P, P, i32, P, P, P, P, P]
+        L.hjcd_mmd.argtypes = [P, i32, P, i32, i32, i32, P, P, P]
         L.hjcd_select_replicate.argtypes = [P, P, P, P, i32, P, P, P]
         L.hjcd_pjik.argtypes = [P, P, P, i32, P, P, P, P, P, P, P]
         L.hjcd_select_best.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P]
@@ -263,6 +267,58 @@ def solve(robot: Robot, targets, cfg: Optional[hjcd_config] = None, out=None,
                                   _ptr(oe), _ptr(st), _ptr(ws), ws.numel(), _stream(stream), evp),
            "hjcd_solve")
     return q, pe, oe, st
+
+
+def solve_batch(robot: Robot, targets, N: int, cfg: Optional[hjcd_config] = None,
+                workspace: Optional[Workspace] = None, stream=None):
+    """The best N polished solutions per target (hjcd_solve_batch): returns
+    (q [T, N, dof], pos_err [T, N], ori_err [T, N], status [T]); entry 0 is
+    hjcd_solve's answer."""
+    torch = _torch()
+    cfg = cfg or default_config()
+    T = targets.shape[0]
+    _dev_f32(targets, (T, 7), "targets")
+    dev = targets.device
+    q = torch.empty((T, N, robot.dof), dtype=torch.float32, device=dev)
+    pe = torch.empty((T, N), dtype=torch.float32, device=dev)
+    oe = torch.empty((T, N), dtype=torch.float32, device=dev)
+    st = torch.empty(T, dtype=torch.int32, device=dev)
+    nbytes = workspace_size(robot, T, cfg)
+    ws = _ws_for(dev, nbytes, workspace)
+    _check(lib().hjcd_solve_batch(robot.handle, C.byref(cfg), _ptr(targets), T, N, _ptr(q), _ptr(pe), _ptr(oe),
+                                  _ptr(st), _ptr(ws), ws.numel(), _stream(stream)), "hjcd_solve_batch")
+    return q, pe, oe, st
+
+
+def select_topn(robot: Robot, cfg: hjcd_config, targets, theta, ep, eo, N: int, stream=None):
+    """Best N of the B polished seeds: theta [T, B, n], ep/eo [T, B] -> (q [T, N, n],
+    pos_err [T, N], ori_err [T, N], idx [T, N])."""
+    torch = _torch()
+    T, n = targets.shape[0], robot.dof
+    _dev_f32(targets, (T, 7), "targets")
+    _dev_f32(theta, (T, cfg.B, n), "theta")
+    d = targets.device
+    q = torch.empty((T, N, n), dtype=torch.float32, device=d)
+    pe = torch.empty((T, N), dtype=torch.float32, device=d)
+    oe = torch.empty((T, N), dtype=torch.float32, device=d)
+    idx = torch.empty((T, N), dtype=torch.int32, device=d)
+    _check(lib().hjcd_select_topn(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(theta), _ptr(ep), _ptr(eo), N,
+                                  _ptr(q), _ptr(pe), _ptr(oe), _ptr(idx), _stream(stream)), "hjcd_select_topn")
+    return q, pe, oe, idx
+
+
+def mmd(X, Y, stream=None):
+    """Per-target MMD^2 (RBF, median-heuristic bandwidth; hjcd_mmd) of X [T, N, d]
+    vs Y [T, N2, d] (cuda f32) -> (mmd2 [T], bandwidth [T])."""
+    torch = _torch()
+    T, N, dim = X.shape
+    N2 = Y.shape[1]
+    _dev_f32(X, (T, N, dim), "X")
+    _dev_f32(Y, (T, N2, dim), "Y")
+    m2 = torch.empty(T, dtype=torch.float32, device=X.device)
+    bw = torch.empty(T, dtype=torch.float32, device=X.device)
+    _check(lib().hjcd_mmd(_ptr(X), N, _ptr(Y), N2, dim, T, _ptr(m2), _ptr(bw), _stream(stream)), "hjcd_mmd")
+    return m2, bw
 
 
 def solve_host(robot: Robot, targets_host, cfg: Optional[hjcd_config] = None, out=None,

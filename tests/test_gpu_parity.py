@@ -310,6 +310,45 @@ def test_pjik_zero_error_fixed_point(hjcd_lib, cuda):
     assert np.array_equal(N(out["theta"]), seeds)
 
 
+# ---------------------------------------------------------------- solution batch + MMD (f2)
+def test_select_topn_and_solve_batch(hjcd_lib, cuda):
+    ch = inputs.panda()
+    rb = hjcd_lib.Robot(ch)
+    tg, th0 = targets_for(ch, 8)
+    p = params(M=256, K=16, B=48, target_early_exit=0)
+    cfg = hjcd_lib.config_from_params(p)
+    seeds = inputs.near_configs(ch, np.repeat(th0[:, None, :], 48, 1), 0.2, seed=2).astype(np.float32)
+    o2 = hjcd_lib.pjik(rb, cfg, T(tg, cuda), T(seeds, cuda))
+    q, pe, oe, idx = hjcd_lib.select_topn(rb, cfg, T(tg, cuda), o2["theta"], o2["ep"], o2["eo"], 20)
+    ref = oracle.select_topn(p, N(o2["ep"]).astype(np.float64), N(o2["eo"]).astype(np.float64), 20)
+    assert np.array_equal(N(idx), ref)
+    assert np.array_equal(N(q), N(o2["theta"])[np.arange(8)[:, None], ref])
+    # the batch API: entry 0 is hjcd_solve's answer, the rest are ordered (R27)
+    qb, peb, oeb, stb = hjcd_lib.solve_batch(rb, T(tg, cuda), 10, cfg)
+    q1, pe1, oe1, st1 = hjcd_lib.solve(rb, T(tg, cuda), cfg)
+    assert np.array_equal(N(qb)[:, 0], N(q1)) and np.array_equal(N(stb), N(st1))
+    c = N(peb).astype(np.float64) ** 2 + 0.25 * N(oeb).astype(np.float64) ** 2
+    conv = (N(peb) < 1e-6) & (N(oeb) < 1e-5)
+    key = np.where(conv, 0.0, 1e9) + c
+    assert np.all(np.diff(key, axis=1) >= 0)
+
+
+@pytest.mark.parametrize("N1,N2,dim", [(50, 50, 7), (1, 1, 3), (13, 40, 14), (128, 128, 8)])
+def test_mmd_parity(hjcd_lib, cuda, N1, N2, dim):
+    rng = np.random.default_rng(N1 + N2 + dim)
+    Tn = 5
+    X = rng.normal(size=(Tn, N1, dim)).astype(np.float32)
+    Y = (rng.normal(size=(Tn, N2, dim)) + 0.3 * np.arange(Tn)[:, None, None]).astype(np.float32)
+    m2, bw = hjcd_lib.mmd(T(X, cuda), T(Y, cuda))
+    for t in range(Tn):
+        r2, h = oracle.mmd2(X[t], Y[t])
+        assert abs(N(bw)[t] - h) <= 1e-6 * h
+        assert abs(N(m2)[t] - r2) <= 1e-6 + 1e-5 * abs(r2), (t, N(m2)[t], r2)
+    # identical sets -> 0
+    z, _ = hjcd_lib.mmd(T(X, cuda), T(X, cuda))
+    assert np.abs(N(z)).max() < 1e-6
+
+
 # ---------------------------------------------------------------- end to end
 def success(pe, oe):
     return (pe < 1e-3) & (oe < math.pi / 180)

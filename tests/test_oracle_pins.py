@@ -533,6 +533,53 @@ def test_ccd_converges_to_closed_form_planar_ik():
     assert np.all(r["ep"] <= r0["ep"] + 1e-12)
 
 
+# ---------------------------------------------------------------- MMD (Table III; R36)
+def test_mmd_single_points_closed_form():
+    # X = {x}, Y = {y}: the one pairwise distance d is the median, so
+    # MMD^2 = k(x,x) + k(y,y) - 2 k(x,y) = 2 - 2 exp(-d^2 / (2 d^2)) = 2 - 2 e^{-1/2}
+    m2, h = oracle.mmd2(np.array([[0.3, -1.0, 2.0]]), np.array([[1.1, 0.5, -0.2]]))
+    assert abs(m2 - (2 - 2 * math.exp(-0.5))) < 1e-15
+    assert abs(h - math.sqrt(0.8 ** 2 + 1.5 ** 2 + 2.2 ** 2)) < 1e-15
+
+
+def test_mmd_identity_symmetry_and_separation():
+    rng = np.random.default_rng(5)
+    X = rng.normal(size=(20, 7))
+    assert abs(oracle.mmd2(X, X)[0]) < 1e-12
+    Y = rng.normal(size=(25, 7))
+    assert abs(oracle.mmd2(X, Y)[0] - oracle.mmd2(Y, X)[0]) < 1e-12
+    # two tight clusters: separated clusters score far above co-located ones.
+    # (The median-heuristic bandwidth grows with the separation, so MMD^2 is NOT
+    # monotone in it: ~0.82 at 10 sigma-units vs ~1.05 at 1.)
+    base = rng.normal(scale=0.1, size=(20, 3))
+    vals = [oracle.mmd2(base, base + np.array([sep, 0, 0]) + rng.normal(scale=0.1, size=(20, 3)))[0]
+            for sep in (10.0, 5.0, 2.0, 1.0, 0.0)]
+    assert min(vals[:-1]) > 0.5 and 0 <= vals[-1] < 0.1, vals
+
+
+def test_mmd_against_kernel_matrix_form():
+    # the same estimator written as 1^T K 1 block means of the (N+N2)^2 Gram matrix
+    rng = np.random.default_rng(9)
+    X, Y = rng.normal(size=(6, 4)), rng.normal(loc=0.5, size=(9, 4))
+    Z = np.concatenate([X, Y])
+    D = np.sqrt(((Z[:, None] - Z[None]) ** 2).sum(-1))
+    h = np.median(D[np.triu_indices(len(Z), 1)])
+    K = np.exp(-D ** 2 / (2 * h * h))
+    ref = K[:6, :6].mean() + K[6:, 6:].mean() - 2 * K[:6, 6:].mean()
+    m2, hh = oracle.mmd2(X, Y)
+    assert abs(m2 - ref) < 1e-13 and abs(hh - h) < 1e-15
+
+
+def test_select_topn_order():
+    p = params(B=7, K=7)
+    ep = np.array([[1e-7, 2e-3, 5e-7, 1e-7, np.nan, 3e-3, 9e-7]])
+    eo = np.array([[1e-6, 1e-3, 2e-6, 1e-6, 0.0, 1e-3, 1e-6]])
+    # converged (ep < 1e-6, eo < 1e-5): slots 0, 2, 3, 6 by c = ep^2 + eo^2/4:
+    # 0 and 3 tie (2.6e-13, lower slot first), 6 (1.06e-12), 2 (1.25e-12);
+    # then 1 (4.25e-6), 5 (9.25e-6), and the NaN slot 4 last
+    assert list(oracle.select_topn(p, ep, eo, 7)[0]) == [0, 3, 6, 2, 1, 5, 4]
+
+
 # ---------------------------------------------------------------- P15 PJ-IK special cases
 def test_pjik_zero_error_fixed_point_and_convergence():
     ch = inputs.panda()
