@@ -186,12 +186,9 @@ cudaError_t launch_mmd(const float* X, int N, const float* Y, int N2, int n, int
                        cudaStream_t s) {
     int Ppad;
     const size_t smem = mmd_smem_bytes(N, N2, n, &Ppad);
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_mmd, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    // N + N2 <= 256 keeps this <= 128 KB + 32 KB (the launch checks the opt-in limit)
+    cudaError_t e = cudaFuncSetAttribute(k_mmd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     k_mmd<<<T, 512, smem, s>>>(X, N, Y, N2, n, Ppad, mmd2, bw);
     return cudaGetLastError();
 }

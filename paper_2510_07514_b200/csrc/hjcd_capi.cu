@@ -26,6 +26,7 @@ thread_local std::string g_cuda_err;
 
 hjcd_status cuda_fail(cudaError_t e) {
     g_cuda_err = cudaGetErrorString(e);
+    (void)cudaGetLastError();   // clear a non-sticky error so the next call does not inherit it
     return HJCD_E_CUDA;
 }
 
