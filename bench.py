@@ -347,6 +347,31 @@ def main():
                           "solves_per_s": Ts / (lat[len(lat) // 2] / 1e3),
                           "success": float((r[3] <= 1).float().mean())})
 
+    # ---------------- DoF sweep (PAPER Table II protocol): Panda
+    # extended cyclically to 7/12/18/24 DoF (R34), 1000 targets, same M/K/B
+    dof_sweep = []
+    if not args.no_sweep and world == 1:
+        for nd in (7, 12, 18, 24):
+            ch = inputs.robot(f"panda_x{nd}")
+            rbd = hjcd.Robot(ch)
+            ths = torch.from_numpy(inputs.halton_configs(ch, 1000).astype(np.float32)).to(dev)
+            tgs = hjcd.fk(rbd, ths).contiguous()
+            c2 = hjcd.default_config(M=M, K=K, B=B)
+            sws = hjcd.Workspace()
+            hjcd.solve(rbd, tgs, c2, workspace=sws)
+            lat = []
+            for _ in range(5):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                r = hjcd.solve(rbd, tgs, c2, workspace=sws)
+                b.record(stream)
+                b.synchronize()
+                lat.append(a.elapsed_time(b))
+            lat.sort()
+            dof_sweep.append({"dof": nd, "targets": 1000, "p50_ms": lat[2], "solves_per_s": 1000 / (lat[2] / 1e3),
+                              "success": float((r[3] <= 1).float().mean()),
+                              "fine_converged": float((r[3] == 0).float().mean())})
+
     # ---------------- end to end through the C ABI with host buffers
     tg_host = targets.cpu().pin_memory()
     outh = (torch.empty((Tg, n), dtype=torch.float32).pin_memory(), torch.empty(Tg).pin_memory(),
@@ -386,6 +411,7 @@ def main():
                "latency_note": "p50/p99 of the per-step batch latency (one hjcd_solve of all targets)",
                "success_rate_1mm_1deg": succ,
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "latency_vs_batch": sweep,
+               "dof_sweep": dof_sweep,
                "gpu_launches": 4 * args.steps, "clocks": clk.summary(),
                "paper_context": "RTX 4060 Laptop, Panda M=1000: 7.53 ms per target (133 targets/s), PAPER.md P:355"}
         print(json.dumps(res))

@@ -168,6 +168,17 @@ hjcd_status hjcd_solve_batch(const hjcd_robot* r, const hjcd_config* c, const fl
                              int32_t N, float* q_out, float* pos_err, float* ori_err, int32_t* status,
                              void* workspace, size_t workspace_bytes, hjcd_stream_t stream);
 
+/* fp64 polish (R29b): PO-CCD, top-K and replication
+ * in fp32 as hjcd_solve (stage 1 only needs the coarse tolerance), then PJ-IK
+ * and best-select in fp64 on an fp64 copy of the chain, so the fine tolerances
+ * can go to SPEC's 1e-9 m / 1e-8 rad.  Outputs are fp64: q_out [T][dof],
+ * pos_err/ori_err [T] (device); status [T] as hjcd_solve.  Workspace: device,
+ * >= hjcd_workspace_size_f64 bytes, 256-byte aligned. */
+hjcd_status hjcd_workspace_size_f64(const hjcd_robot* r, int32_t T, const hjcd_config* c, size_t* bytes);
+hjcd_status hjcd_solve_f64(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                           double* q_out, double* pos_err, double* ori_err, int32_t* status,
+                           void* workspace, size_t workspace_bytes, hjcd_stream_t stream);
+
 /* The same with HOST buffers (same shapes): copies targets host->device,
  * solves, copies results device->host, and synchronises `stream` before
  * returning.  workspace: device, >= hjcd_workspace_size_host bytes. */
@@ -226,6 +237,13 @@ hjcd_status hjcd_select_best(const hjcd_robot* r, const hjcd_config* c, const fl
                              int32_t T, const float* theta, const float* pos_err_all,
                              const float* ori_err_all, float* q_out, float* pos_err,
                              float* ori_err, int32_t* status, hjcd_stream_t stream);
+
+/* PJ-IK (Alg. 4) in fp64 (the stage of hjcd_solve_f64): fp32 seeds [T][B][dof]
+ * in; theta [T][B][dof], pos_err/ori_err [T][B] fp64 out; step_counts and
+ * iters as hjcd_pjik. */
+hjcd_status hjcd_pjik_f64(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                          const float* seeds, double* theta, double* pos_err, double* ori_err,
+                          int32_t* step_counts, int32_t* iters, hjcd_stream_t stream);
 
 /* Best N of the B polished seeds per target (the stage of hjcd_solve_batch):
  * theta [T][B][dof], pos_err_all/ori_err_all [T][B] in; q_out [T][N][dof],

@@ -19,19 +19,28 @@ cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targe
     return launch_poccd_t<32, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
 }
 
-cudaError_t launch_pjik_coop(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
-                             const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
-                             int32_t* iters, cudaStream_t s) {
+template <class T>
+cudaError_t launch_pjik_coop(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
+                             const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
+                             cudaStream_t s) {
     if (c.copies * c.K > 256 || 2 * c.A + 2 > 64) return cudaErrorInvalidConfiguration;
     switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
-        case 7: return launch_coop_t<7, true>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
-        case 8: return launch_coop_t<8, true>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
-        case 14: return launch_coop_t<14, true>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+        case 7: return launch_coop_t<T, 7, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+        case 8: return launch_coop_t<T, 8, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+        case 14: return launch_coop_t<T, 14, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
         default: break;
     }
-    if (rb.n <= 8) return launch_coop_t<8, false>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
-    if (rb.n <= 16) return launch_coop_t<16, false>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
-    return launch_coop_t<32, false>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+    if (rb.n <= 8) return launch_coop_t<T, 8, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+    if (rb.n <= 16) return launch_coop_t<T, 16, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+    return launch_coop_t<T, 32, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+}
+template cudaError_t launch_pjik_coop<float>(const DevRobotT<float>&, const DevCfg&, const float*, int, const float*,
+                                             float*, float*, float*, int32_t*, int32_t*, cudaStream_t);
+
+cudaError_t launch_pjik64(const DevRobotT<double>& rb, const DevCfg& c, const float* targets, int T,
+                          const float* seeds, double* theta, double* ep, double* eo, int32_t* counts,
+                          int32_t* iters, cudaStream_t s) {
+    return launch_pjik_coop<double>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
 }
 
 cudaError_t launch_pjik(const DevRobot& rb, const DevCfg& c, const float* targets, int T,

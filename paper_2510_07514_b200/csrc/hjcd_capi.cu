@@ -18,6 +18,7 @@ struct hjcd_robot {
     double ee_quat[4];
     int dof;
     DevRobot dev;
+    DevRobotT<double> dev64;   // the same chain in fp64 (hjcd_solve_f64)
 };
 
 namespace {
@@ -89,9 +90,10 @@ Rt rot_z_to(const double a[3]) {
     return C;
 }
 
-void store(const Rt& a, float R[9], float t[3]) {
-    for (int i = 0; i < 9; ++i) R[i] = (float)a.R[i];
-    for (int i = 0; i < 3; ++i) t[i] = (float)a.t[i];
+template <class S>
+void store(const Rt& a, S R[9], S t[3]) {
+    for (int i = 0; i < 9; ++i) R[i] = (S)a.R[i];
+    for (int i = 0; i < 3; ++i) t[i] = (S)a.t[i];
 }
 
 bool finite3(const double* v, int k) {
@@ -136,7 +138,9 @@ hjcd_status build_robot(const hjcd_joint* joints, int32_t num, const double ee_x
     for (int i = 0; i < 4; ++i) r->ee_quat[i] = ee_quat[i];
     r->dof = dof;
     std::memset(&r->dev, 0, sizeof(DevRobot));
+    std::memset(&r->dev64, 0, sizeof(r->dev64));
     r->dev.n = dof;
+    r->dev64.n = dof;
     // Canonicalise: Rot(a, th) = C Rz(th) C^T with C e_z = a; fold C^T and any
     // fixed joints into the next joint's fixed transform F (or the ee).
     Rt acc = rt_identity();
@@ -154,11 +158,18 @@ hjcd_status build_robot(const hjcd_joint* joints, int32_t num, const double ee_x
         dj.lo = (float)j.lo;
         dj.hi = (float)j.hi;
         dj.type = j.type;
+        DevJointT<double>& dd = r->dev64.j[d];
+        store(F, dd.R, dd.t);
+        // fp64 limits = the fp32 ones widened, so both precisions clamp to the same box
+        dd.lo = (double)dj.lo;
+        dd.hi = (double)dj.hi;
+        dd.type = j.type;
         acc = rt_transpose_rot(C);
         d++;
     }
     Rt E = rt_mul(acc, rt_from_pose(ee_xyz, ee_quat));
     store(E, r->dev.eeR, r->dev.eet);
+    store(E, r->dev64.eeR, r->dev64.eet);
     *out = r;
     return HJCD_OK;
 }
@@ -215,6 +226,23 @@ Layout layout(int dof, long long T, const hjcd_config* c) {
     L.seeds2 = off; off += align256((size_t)T * c->B * dof * sizeof(float));
     L.ep2 = off;    off += align256((size_t)T * c->B * sizeof(float));
     L.eo2 = off;    off += align256((size_t)T * c->B * sizeof(float));
+    L.total = off;
+    return L;
+}
+
+struct Layout64 {
+    size_t theta1, cost1, seeds2, theta64, ep64, eo64, total;
+};
+
+Layout64 layout64(int dof, long long T, const hjcd_config* c) {
+    Layout64 L;
+    size_t off = 0;
+    L.theta1 = off;  off += align256((size_t)T * dof * c->M * sizeof(float));
+    L.cost1 = off;   off += align256((size_t)T * c->M * sizeof(float));
+    L.seeds2 = off;  off += align256((size_t)T * c->B * dof * sizeof(float));
+    L.theta64 = off; off += align256((size_t)T * c->B * dof * sizeof(double));
+    L.ep64 = off;    off += align256((size_t)T * c->B * sizeof(double));
+    L.eo64 = off;    off += align256((size_t)T * c->B * sizeof(double));
     L.total = off;
     return L;
 }
@@ -371,6 +399,60 @@ hjcd_status hjcd_solve_batch(const hjcd_robot* r, const hjcd_config* c, const fl
                                 s)) != cudaSuccess)
         return cuda_fail(e);
     return HJCD_OK;
+}
+
+hjcd_status hjcd_workspace_size_f64(const hjcd_robot* r, int32_t T, const hjcd_config* c, size_t* bytes) {
+    if (!r || !c || !bytes || T < 1) return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    if ((st = check_poccd(c)) != HJCD_OK) return st;
+    *bytes = layout64(r->dof, T, c).total;
+    return HJCD_OK;
+}
+
+hjcd_status hjcd_solve_f64(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                           double* q_out, double* pos_err, double* ori_err, int32_t* status, void* workspace,
+                           size_t workspace_bytes, hjcd_stream_t stream) {
+    if (!r || !c || !targets || T < 1 || !q_out || !pos_err || !ori_err || !status || !workspace)
+        return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    if (c->M > 8192) return HJCD_E_UNSUPPORTED;
+    if ((st = check_poccd(c)) != HJCD_OK) return st;
+    Layout64 L = layout64(r->dof, T, c);
+    if (workspace_bytes < L.total || ((uintptr_t)workspace & 255)) return HJCD_E_WORKSPACE;
+    char* ws = (char*)workspace;
+    float* theta1 = (float*)(ws + L.theta1);
+    float* cost1 = (float*)(ws + L.cost1);
+    float* seeds2 = (float*)(ws + L.seeds2);
+    double* th64 = (double*)(ws + L.theta64);
+    double* ep64 = (double*)(ws + L.ep64);
+    double* eo64 = (double*)(ws + L.eo64);
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    // stage 1 and the hand-over in fp32 (PO-CCD only needs the coarse
+    // tolerance), stage 2 and the answer in fp64 on the fp64 chain (f1)
+    if ((e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s)) != cudaSuccess ||
+        (e = launch_select_replicate(r->dev, d, cost1, theta1, T, seeds2, nullptr, s)) != cudaSuccess ||
+        (e = launch_pjik64(r->dev64, d, targets, T, seeds2, th64, ep64, eo64, nullptr, nullptr, s)) != cudaSuccess ||
+        (e = launch_select_best(r->dev, d, targets, T, (const double*)th64, (const double*)ep64, (const double*)eo64,
+                                q_out, pos_err, ori_err, status, s)) != cudaSuccess)
+        return cuda_fail(e);
+    return HJCD_OK;
+}
+
+hjcd_status hjcd_pjik_f64(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                          const float* seeds, double* theta, double* pos_err, double* ori_err, int32_t* step_counts,
+                          int32_t* iters, hjcd_stream_t stream) {
+    if (!r || !c || !targets || T < 1 || !seeds || !theta || !pos_err || !ori_err) return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    cudaError_t e = launch_pjik64(r->dev64, d, targets, T, seeds, theta, pos_err, ori_err, step_counts, iters,
+                                  (cudaStream_t)stream);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
 }
 
 hjcd_status hjcd_select_topn(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,

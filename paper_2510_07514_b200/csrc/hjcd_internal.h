@@ -12,26 +12,30 @@
 
 namespace hjcd {
 
-// One DoF joint after canonicalisation (host, fp64 -> fp32):
+// One DoF joint after canonicalisation (host, fp64 -> S):
 //   T_i = T_{i-1} * F_i * Rz(theta_i)        (revolute)
 //   T_i = T_{i-1} * F_i * Tz(theta_i)        (prismatic)
 // F_i = [R | t] (R row-major).  P_i = translation of T_{i-1} F_i, z_i = its
 // third rotation column, which equal the paper's P_i, z_i (Eq. 7).
-struct DevJoint {
-    float R[9];
-    float t[3];
-    float lo, hi;
+template <class S>
+struct DevJointT {
+    S R[9];
+    S t[3];
+    S lo, hi;
     int32_t type;  // HJCD_REVOLUTE / HJCD_PRISMATIC
     int32_t pad;
 };
 
-struct DevRobot {
+template <class S>
+struct DevRobotT {
     int32_t n;
     int32_t pad[3];
-    DevJoint j[HJCD_MAX_DOF];
-    float eeR[9];
-    float eet[3];
+    DevJointT<S> j[HJCD_MAX_DOF];
+    S eeR[9];
+    S eet[3];
 };
+using DevJoint = DevJointT<float>;
+using DevRobot = DevRobotT<float>;   // the fp32 kernels; DevRobotT<double> for the fp64 polish
 
 struct DevCfg {
     int32_t M, K, B, ccd_iters, lm_iters, A, copies, repl_noise_all, target_early_exit, ccd_early_exit;
@@ -56,10 +60,10 @@ cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* tar
 template <int NMAX, bool EXACT>
 cudaError_t launch_ccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* seeds,
                          float* theta, float* ep, int32_t* iters, cudaStream_t s);
-template <int NMAX, bool EXACT>
-cudaError_t launch_coop_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
-                          const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
-                          int32_t* iters, cudaStream_t s);
+template <class T, int NMAX, bool EXACT>
+cudaError_t launch_coop_t(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
+                          const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
+                          cudaStream_t s);
 
 // launchers (dispatch.cu, select.cu); all asynchronous on `s`
 cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, float* jac,
@@ -75,17 +79,22 @@ cudaError_t launch_select_replicate(const DevRobot& rb, const DevCfg& c, const f
 cudaError_t launch_pjik(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                         const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
                         int32_t* iters, cudaStream_t s);
-cudaError_t launch_pjik_coop(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
-                             const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
-                             int32_t* iters, cudaStream_t s);
+template <class T>
+cudaError_t launch_pjik_coop(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
+                             const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
+                             cudaStream_t s);
 cudaError_t launch_select_topn(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* theta,
                                const float* ep_all, const float* eo_all, int N, float* q_out, float* pos_err,
                                float* ori_err, int32_t* idx, int32_t* status, cudaStream_t s);
 cudaError_t launch_mmd(const float* X, int N, const float* Y, int N2, int n, int T, float* mmd2, float* bw,
                        cudaStream_t s);
-cudaError_t launch_select_best(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
-                               const float* theta, const float* ep_all, const float* eo_all,
-                               float* q_out, float* pos_err, float* ori_err, int32_t* status,
-                               cudaStream_t s);
+template <class T>
+cudaError_t launch_select_best(const DevRobot& rb, const DevCfg& c, const float* targets, int T_,
+                               const T* theta, const T* ep_all, const T* eo_all, T* q_out, T* pos_err,
+                               T* ori_err, int32_t* status, cudaStream_t s);
+// fp64 polish: the same PJ-IK on DevRobotT<double>
+cudaError_t launch_pjik64(const DevRobotT<double>& rb, const DevCfg& c, const float* targets, int T,
+                          const float* seeds, double* theta, double* ep, double* eo, int32_t* counts,
+                          int32_t* iters, cudaStream_t s);
 
 }  // namespace hjcd

@@ -1,0 +1,6 @@
+// inst_coop64_16.cu — explicit instantiation(s) of the cooperative PJ-IK launcher, double (see dispatch.cu)
+#include "pjik_coop.cuh"
+
+namespace hjcd {
+template cudaError_t launch_coop_t<double, 16, false>(const DevRobotT<double>&, const DevCfg&, const float*, int, const float*, double*, double*, double*, int32_t*, int32_t*, cudaStream_t);
+}  // namespace hjcd

@@ -1,6 +1,6 @@
-// inst_coop_16.cu — explicit instantiation(s) of the pjik_coop.cuh launcher (see dispatch.cu)
+// inst_coop_16.cu — explicit instantiation(s) of the cooperative PJ-IK launcher, float (see dispatch.cu)
 #include "pjik_coop.cuh"
 
 namespace hjcd {
-template cudaError_t launch_coop_t<16, false>(const DevRobot&, const DevCfg&, const float*, int, const float*, float*, float*, float*, int32_t*, int32_t*, cudaStream_t);
+template cudaError_t launch_coop_t<float, 16, false>(const DevRobotT<float>&, const DevCfg&, const float*, int, const float*, float*, float*, float*, int32_t*, int32_t*, cudaStream_t);
 }  // namespace hjcd

@@ -12,11 +12,25 @@
 
 namespace hjcd {
 
-struct Quat {
-    float w, x, y, z;
+// ---------------------------------------------------------------- precision
+// The polish stage runs in fp32 (the default) or fp64 (hjcd_solve_f64, SURVEY
+// §8(f) f1); everything it uses is templated on the scalar R.  vec3<R> is
+// float3 / double3; the float forms are the ones the fp32 kernels always used.
+template <class R> struct VecT;
+template <> struct VecT<float> { using type = float3; };
+template <> struct VecT<double> { using type = double3; };
+template <class R> using vec3 = typename VecT<R>::type;
+
+template <class R>
+struct QuatT {
+    R w, x, y, z;
 };
+using Quat = QuatT<float>;
 
 __device__ __forceinline__ float3 f3(float x, float y, float z) { return make_float3(x, y, z); }
+__device__ __forceinline__ double3 f3(double x, double y, double z) { return make_double3(x, y, z); }
+template <class R>
+__device__ __forceinline__ vec3<R> mk3(R x, R y, R z) { return f3(x, y, z); }
 __device__ __forceinline__ float3 operator+(float3 a, float3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }
 __device__ __forceinline__ float3 operator-(float3 a, float3 b) { return f3(a.x - b.x, a.y - b.y, a.z - b.z); }
 __device__ __forceinline__ float3 operator*(float s, float3 a) { return f3(s * a.x, s * a.y, s * a.z); }
@@ -24,11 +38,20 @@ __device__ __forceinline__ float dot3(float3 a, float3 b) { return a.x * b.x + a
 __device__ __forceinline__ float3 cross3(float3 a, float3 b) {
     return f3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
 }
+__device__ __forceinline__ double3 operator+(double3 a, double3 b) { return f3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ double3 operator-(double3 a, double3 b) { return f3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ double3 operator*(double s, double3 a) { return f3(s * a.x, s * a.y, s * a.z); }
+__device__ __forceinline__ double dot3(double3 a, double3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ double3 cross3(double3 a, double3 b) {
+    return f3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
 __device__ __forceinline__ float clampf(float x, float lo, float hi) { return fminf(fmaxf(x, lo), hi); }
+__device__ __forceinline__ double clampf(double x, double lo, double hi) { return fmin(fmax(x, lo), hi); }
 
 // Hamilton product a (x) conj(b)
-__device__ __forceinline__ Quat qmul_conj(Quat a, Quat b) {
-    Quat r;
+template <class R>
+__device__ __forceinline__ QuatT<R> qmul_conj(QuatT<R> a, QuatT<R> b) {
+    QuatT<R> r;
     r.w = a.w * b.w + a.x * b.x + a.y * b.y + a.z * b.z;
     r.x = -a.w * b.x + a.x * b.w - a.y * b.z + a.z * b.y;
     r.y = -a.w * b.y + a.x * b.z + a.y * b.w - a.z * b.x;
@@ -37,9 +60,10 @@ __device__ __forceinline__ Quat qmul_conj(Quat a, Quat b) {
 }
 
 // q_err = q_t (x) q_e^-1, canonicalised to w >= 0 (Eq. 5; reading R1)
-__device__ __forceinline__ Quat quat_err(Quat qt, Quat qe) {
-    Quat q = qmul_conj(qt, qe);
-    if (q.w < 0.f) { q.w = -q.w; q.x = -q.x; q.y = -q.y; q.z = -q.z; }
+template <class R>
+__device__ __forceinline__ QuatT<R> quat_err(QuatT<R> qt, QuatT<R> qe) {
+    QuatT<R> q = qmul_conj(qt, qe);
+    if (q.w < R(0)) { q.w = -q.w; q.x = -q.x; q.y = -q.y; q.z = -q.z; }
     return q;
 }
 
@@ -65,28 +89,33 @@ __device__ __forceinline__ Quat qerr_rotate(Quat q, float3 z, float c2, float s2
 // branches: the four pivots 4q_i^2 = t_i are formed, the largest is chosen by
 // selects, and q = (column of the symmetric 4x4 form) * rsqrt(t)/2.  Seeds of
 // a warp sit in different quadrants, so the branchy form diverges 4 ways.
-__device__ __forceinline__ Quat quat_from_rot(const float R[9]) {
-    const float t0 = 1.f + R[0] + R[4] + R[8];   // 4 w^2
-    const float t1 = 1.f + R[0] - R[4] - R[8];   // 4 x^2
-    const float t2 = 1.f - R[0] + R[4] - R[8];   // 4 y^2
-    const float t3 = 1.f - R[0] - R[4] + R[8];   // 4 z^2
-    const float a = R[7] - R[5], b = R[2] - R[6], cc = R[3] - R[1];   // 4wx, 4wy, 4wz
-    const float d = R[1] + R[3], e = R[2] + R[6], f = R[5] + R[7];    // 4xy, 4xz, 4yz
+__device__ __forceinline__ float rsqrt_q(float x) { return rsqrtf(x); }
+__device__ __forceinline__ double rsqrt_q(double x) { return 1.0 / sqrt(x); }
+
+template <class T>
+__device__ __forceinline__ QuatT<T> quat_from_rot(const T R[9]) {
+    const T one = T(1);
+    const T t0 = one + R[0] + R[4] + R[8];   // 4 w^2
+    const T t1 = one + R[0] - R[4] - R[8];   // 4 x^2
+    const T t2 = one - R[0] + R[4] - R[8];   // 4 y^2
+    const T t3 = one - R[0] - R[4] + R[8];   // 4 z^2
+    const T a = R[7] - R[5], b = R[2] - R[6], cc = R[3] - R[1];   // 4wx, 4wy, 4wz
+    const T d = R[1] + R[3], e = R[2] + R[6], f = R[5] + R[7];    // 4xy, 4xz, 4yz
     // same branch order as the classic form: w if tr > 0, else the largest diagonal
-    const bool pw = (R[0] + R[4] + R[8]) > 0.f;
+    const bool pw = (R[0] + R[4] + R[8]) > T(0);
     const bool px = !pw && R[0] > R[4] && R[0] > R[8];
     const bool py = !pw && !px && R[4] > R[8];
-    float t, qw, qx, qy, qz;   // the pivot's column, scaled by 4 q_pivot
+    T t, qw, qx, qy, qz;   // the pivot's column, scaled by 4 q_pivot
     if (pw) { t = t0; qw = t0; qx = a; qy = b; qz = cc; }
     else if (px) { t = t1; qw = a; qx = t1; qy = d; qz = e; }
     else if (py) { t = t2; qw = b; qx = d; qy = t2; qz = f; }
     else { t = t3; qw = cc; qx = e; qy = f; qz = t3; }
-    const float is = 0.5f * rsqrtf(t);
-    Quat q;
+    const T is = T(0.5) * rsqrt_q(t);
+    QuatT<T> q;
     q.w = qw * is; q.x = qx * is; q.y = qy * is; q.z = qz * is;
     // renormalise (absorbs the rsqrt approximation and FK rounding)
-    float inv = rsqrtf(q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z);
-    if (q.w < 0.f) inv = -inv;
+    T inv = rsqrt_q(q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z);
+    if (q.w < T(0)) inv = -inv;
     q.w *= inv; q.x *= inv; q.y *= inv; q.z *= inv;
     return q;
 }
@@ -111,6 +140,7 @@ __device__ __forceinline__ void sincos_b(float x, float* s, float* c) {
     *s = (qi & 2) ? -sa : sa;
     *c = ((qi + 1) & 2) ? -ca : ca;
 }
+__device__ __forceinline__ void sincos_b(double x, double* s, double* c) { sincos(x, s, c); }
 
 // Forward kinematics (Eq. 1) with frames (Eq. 7 inputs):
 // T = F_1 Rz(th_1) F_2 Rz(th_2) ... F_n Rz(th_n) EE  (prismatic: Tz).
@@ -119,35 +149,35 @@ __device__ __forceinline__ void sincos_b(float x, float* s, float* c) {
 // EXACT: the chain has exactly NMAX DoF (no per-joint guard).  FAST: joint
 // sincos on the SFU (__sincosf, |err| <~ 5e-7 rad on the joint ranges): used by
 // the coarse stage only (K5); the polish stage uses sincos_b.
-template <int NMAX, bool FRAMES, bool EXACT = false, bool FAST = false>
-__device__ __forceinline__ void fk(const DevRobot& rb, const float (&th)[NMAX], float3 (&P)[NMAX],
-                                   float3 (&Z)[NMAX], float3& pe, Quat& qe) {
-    float R[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
-    float tx = 0.f, ty = 0.f, tz = 0.f;
+template <int NMAX, bool FRAMES, bool EXACT = false, bool FAST = false, class T>
+__device__ __forceinline__ void fk(const DevRobotT<T>& rb, const T (&th)[NMAX], vec3<T> (&P)[NMAX],
+                                   vec3<T> (&Z)[NMAX], vec3<T>& pe, QuatT<T>& qe) {
+    T R[9] = {T(1), T(0), T(0), T(0), T(1), T(0), T(0), T(0), T(1)};
+    T tx = T(0), ty = T(0), tz = T(0);
 #pragma unroll
     for (int j = 0; j < NMAX; ++j) {
         if (EXACT || j < rb.n) {
-            const DevJoint& J = rb.j[j];
+            const DevJointT<T>& J = rb.j[j];
             tx += R[0] * J.t[0] + R[1] * J.t[1] + R[2] * J.t[2];
             ty += R[3] * J.t[0] + R[4] * J.t[1] + R[5] * J.t[2];
             tz += R[6] * J.t[0] + R[7] * J.t[1] + R[8] * J.t[2];
-            float N[9];
+            T N[9];
 #pragma unroll
             for (int r = 0; r < 3; ++r)
 #pragma unroll
                 for (int cc = 0; cc < 3; ++cc)
                     N[3 * r + cc] = R[3 * r] * J.R[cc] + R[3 * r + 1] * J.R[3 + cc] + R[3 * r + 2] * J.R[6 + cc];
             if (FRAMES) {
-                P[j] = f3(tx, ty, tz);
-                Z[j] = f3(N[2], N[5], N[8]);
+                P[j] = mk3<T>(tx, ty, tz);
+                Z[j] = mk3<T>(N[2], N[5], N[8]);
             }
             if (J.type == HJCD_REVOLUTE) {
-                float s, c;
-                if (FAST) __sincosf(th[j], &s, &c);
+                T s, c;
+                if constexpr (FAST) __sincosf(th[j], &s, &c);
                 else sincos_b(th[j], &s, &c);
 #pragma unroll
                 for (int r = 0; r < 3; ++r) {
-                    float a = N[3 * r], b = N[3 * r + 1];
+                    T a = N[3 * r], b = N[3 * r + 1];
                     R[3 * r] = c * a + s * b;
                     R[3 * r + 1] = c * b - s * a;
                     R[3 * r + 2] = N[3 * r + 2];
@@ -164,13 +194,13 @@ __device__ __forceinline__ void fk(const DevRobot& rb, const float (&th)[NMAX], 
     tx += R[0] * rb.eet[0] + R[1] * rb.eet[1] + R[2] * rb.eet[2];
     ty += R[3] * rb.eet[0] + R[4] * rb.eet[1] + R[5] * rb.eet[2];
     tz += R[6] * rb.eet[0] + R[7] * rb.eet[1] + R[8] * rb.eet[2];
-    float E[9];
+    T E[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int cc = 0; cc < 3; ++cc)
             E[3 * r + cc] = R[3 * r] * rb.eeR[cc] + R[3 * r + 1] * rb.eeR[3 + cc] + R[3 * r + 2] * rb.eeR[6 + cc];
-    pe = f3(tx, ty, tz);
+    pe = mk3<T>(tx, ty, tz);
     qe = quat_from_rot(E);
 }
 
@@ -210,23 +240,29 @@ __device__ __forceinline__ float fast_atan2f(float y, float x) {
 }
 
 // ---------------------------------------------------------------- targets
-struct Target {
-    float3 p;
-    Quat q;
+template <class R>
+struct TargetT {
+    vec3<R> p;
+    QuatT<R> q;
     bool valid;
 };
+using Target = TargetT<float>;
 
-// S2: normalise q when | |q| - 1 | <= 1e-3, else invalid (status 3 later)
-__device__ __forceinline__ Target load_target(const float* __restrict__ t7) {
-    Target t;
-    t.p = f3(__ldg(t7 + 0), __ldg(t7 + 1), __ldg(t7 + 2));
-    float w = __ldg(t7 + 3), x = __ldg(t7 + 4), y = __ldg(t7 + 5), z = __ldg(t7 + 6);
-    float nq = sqrtf(w * w + x * x + y * y + z * z);
-    t.valid = fabsf(nq - 1.f) <= 1e-3f && isfinite(nq) && isfinite(t.p.x) && isfinite(t.p.y) &&
-              isfinite(t.p.z);
-    if (!t.valid) { w = 1.f; x = y = z = 0.f; nq = 1.f; t.p = f3(0.f, 0.f, 0.f); }
-    float inv = 1.f / nq;
-    if (w < 0.f) inv = -inv;
+// S2: normalise q when | |q| - 1 | <= 1e-3 (tested in fp32 at either precision),
+// else invalid (status 3 later).  The fp32 target is widened exactly.
+template <class R = float>
+__device__ __forceinline__ TargetT<R> load_target(const float* __restrict__ t7) {
+    TargetT<R> t;
+    const float px = __ldg(t7 + 0), py = __ldg(t7 + 1), pz = __ldg(t7 + 2);
+    const float w32 = __ldg(t7 + 3), x32 = __ldg(t7 + 4), y32 = __ldg(t7 + 5), z32 = __ldg(t7 + 6);
+    const float nq32 = sqrtf(w32 * w32 + x32 * x32 + y32 * y32 + z32 * z32);
+    t.valid = fabsf(nq32 - 1.f) <= 1e-3f && isfinite(nq32) && isfinite(px) && isfinite(py) && isfinite(pz);
+    R w = w32, x = x32, y = y32, z = z32;
+    R nq = sqrt(w * w + x * x + y * y + z * z);
+    t.p = mk3<R>(px, py, pz);
+    if (!t.valid) { w = R(1); x = y = z = R(0); nq = R(1); t.p = mk3<R>(R(0), R(0), R(0)); }
+    R inv = R(1) / nq;
+    if (w < R(0)) inv = -inv;
     t.q.w = w * inv; t.q.x = x * inv; t.q.y = y * inv; t.q.z = z * inv;
     return t;
 }
@@ -275,15 +311,29 @@ __device__ __forceinline__ void normals4(uint4 r, float g[4]) {
     }
 }
 
+// fp64 polish: the same Box-Muller in fp64 (as the oracle draws them)
+__device__ __forceinline__ void normals4(uint4 r, double g[4]) {
+    const double s23 = 1.1920928955078125e-07;
+    const double u0 = ((double)(r.x >> 9) + 0.5) * s23, u1 = ((double)(r.y >> 9) + 0.5) * s23;
+    const double u2 = ((double)(r.z >> 9) + 0.5) * s23, u3 = ((double)(r.w >> 9) + 0.5) * s23;
+    const double ra = sqrt(-2.0 * log(u0)), rb2 = sqrt(-2.0 * log(u2));
+    double s, c;
+    sincospi(2.0 * u1, &s, &c);
+    g[0] = ra * c; g[1] = ra * s;
+    sincospi(2.0 * u3, &s, &c);
+    g[2] = rb2 * c; g[3] = rb2 * s;
+}
+
 // theta <- clamp(theta + sigma * N(0, I)), stream (tid, sid, purpose, iter)
-template <int NMAX, bool EXACT = false, bool FAST = false>
-__device__ __forceinline__ void perturb(const DevRobot& rb, const DevCfg& c, float (&th)[NMAX], float sigma,
+template <int NMAX, bool EXACT = false, bool FAST = false, class T>
+__device__ __forceinline__ void perturb(const DevRobotT<T>& rb, const DevCfg& c, T (&th)[NMAX], T sigma,
                                         uint32_t tid, uint32_t sid, uint32_t purpose, uint32_t iter) {
 #pragma unroll
     for (int blk = 0; blk < (NMAX + 3) / 4; ++blk) {
         if (EXACT || 4 * blk < rb.n) {
-            float g[4];
-            normals4<FAST>(draw(c, tid, sid, purpose, iter, blk), g);
+            T g[4];
+            if constexpr (sizeof(T) == 4) normals4<FAST>(draw(c, tid, sid, purpose, iter, blk), g);
+            else normals4(draw(c, tid, sid, purpose, iter, blk), g);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 int j = 4 * blk + e;

@@ -21,23 +21,24 @@
 namespace hjcd {
 
 // per-seed shared-memory record, structure-of-arrays with stride = blockDim.x
+template <class T>
 struct CoopSmem {
-    float* th;     // [NMAX][nt]
-    float* dir;    // [3][NMAX][nt]   LM, dogleg, single-coordinate directions
-    float* W;      // [6][nt]
-    float* c0;     // [nt]
-    float* n0;     // [nt]
+    T* th;         // [NMAX][nt]
+    T* dir;        // [3][NMAX][nt]   LM, dogleg, single-coordinate directions
+    T* W;          // [6][nt]
+    T* c0;         // [nt]
+    T* n0;         // [nt]
     int* flags;    // [nt]  bit0 LM, bit1 dogleg, bit2 single
-    int* incl;     // [nt]  inclusive prefix of pending items within the warp
+    int* incl;     // [nt]  inclusive prefix of pending items within the CTA
     unsigned long long* ok;   // [nt]  success bits in cascade order
 };
 
-template <int NMAX>
-__device__ __forceinline__ CoopSmem coop_smem(void* base, int nt) {
-    CoopSmem s;
+template <class T, int NMAX>
+__device__ __forceinline__ CoopSmem<T> coop_smem(void* base, int nt) {
+    CoopSmem<T> s;
     unsigned long long* p64 = (unsigned long long*)base;
     s.ok = p64;
-    float* f = (float*)(p64 + nt);
+    T* f = (T*)(p64 + nt);
     s.th = f; f += NMAX * nt;
     s.dir = f; f += 3 * NMAX * nt;
     s.W = f; f += 6 * nt;
@@ -48,50 +49,49 @@ __device__ __forceinline__ CoopSmem coop_smem(void* base, int nt) {
     return s;
 }
 
-template <int NMAX>
+template <class T, int NMAX>
 size_t coop_smem_bytes(int nt) {
-    return (size_t)nt * (8 + 4 * (4 * NMAX + 6 + 2) + 4 * 2);
+    return (size_t)nt * (8 + sizeof(T) * (4 * NMAX + 6 + 2) + 4 * 2);
 }
 
-
-template <int NMAX, bool EXACT>
+template <class T, int NMAX, bool EXACT>
 __global__ void __launch_bounds__(256)
-k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
+k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ DevCfg c,
             const float* __restrict__ targets, const float* __restrict__ seeds,
-            float* __restrict__ theta_out, float* __restrict__ ep_out, float* __restrict__ eo_out,
+            T* __restrict__ theta_out, T* __restrict__ ep_out, T* __restrict__ eo_out,
             int32_t* __restrict__ counts_out, int32_t* __restrict__ iters_out) {
     extern __shared__ unsigned long long coop_raw[];
     __shared__ int s_wtot[8];   // per-warp item totals (<= 256 threads)
     const int nt = blockDim.x;
-    const CoopSmem S = coop_smem<NMAX>(coop_raw, nt);
+    const CoopSmem<T> S = coop_smem<T, NMAX>(coop_raw, nt);
     const int n = rb.n;
     const int used = c.copies * c.K;
     const int t = blockIdx.x;
     const int b = threadIdx.x;
     const int lane = b & 31;
     const bool active = b < used;
-    const Target tg = load_target(targets + 7ll * t);
+    const TargetT<T> tg = load_target<T>(targets + 7ll * t);
     const uint32_t tid = (uint32_t)(c.tid_offset + t);
     const long long row = (long long)t * c.B + b;
 
-    float th[NMAX], tt[NMAX], dth[NMAX];
+    T th[NMAX], tt[NMAX], dth[NMAX];
 #pragma unroll
-    for (int j = 0; j < NMAX; ++j) th[j] = (active && (EXACT || j < n)) ? seeds[row * n + j] : 0.f;
+    for (int j = 0; j < NMAX; ++j) th[j] = (active && (EXACT || j < n)) ? T(seeds[row * n + j]) : T(0);
 
     int cnt[4] = {0, 0, 0, 0};
-    float3 Jp[NMAX], Jo[NMAX];
-    Resid r;
+    vec3<T> Jp[NMAX], Jo[NMAX];
+    ResidT<T> r;
     bool live = active;   // per-seed mode: cleared when this seed converges
     int kseed = 0;
     int k;
     for (k = 0;; ++k) {
-        float3 pe;
-        Quat qe;
+        vec3<T> pe;
+        QuatT<T> qe;
         bool conv = false;
         if (live) {
             fk<NMAX, true, EXACT>(rb, th, Jp, Jo, pe, qe);
             r = residual(tg, pe, qe);
-            conv = r.ep < c.eps_p_fine && r.eo < c.eps_o_fine;   // Alg. 4 l.18 (R26)
+            conv = r.ep < T(c.eps_p_fine) && r.eo < T(c.eps_o_fine);   // Alg. 4 l.18 (R26)
         }
         if (c.target_early_exit) {
             if (__syncthreads_or(conv)) break;                  // R26b: target stops
@@ -110,30 +110,30 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
 #pragma unroll
             for (int j = 0; j < NMAX; ++j) {
                 if (EXACT || j < n) {
-                    const float3 z = Jo[j];
+                    const vec3<T> z = Jo[j];
                     if (rb.j[j].type == HJCD_REVOLUTE) {
                         Jp[j] = cross3(z, pe - Jp[j]);
                     } else {
                         Jp[j] = z;
-                        Jo[j] = f3(0.f, 0.f, 0.f);
+                        Jo[j] = mk3<T>(T(0), T(0), T(0));
                     }
                 }
             }
-            float W[6], invD[NMAX];
+            T W[6], invD[NMAX];
             {
-                float rn[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                T rn[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
 #pragma unroll
                 for (int j = 0; j < NMAX; ++j) {
                     if (EXACT || j < n) {
                         rn[0] += Jp[j].x * Jp[j].x; rn[1] += Jp[j].y * Jp[j].y; rn[2] += Jp[j].z * Jp[j].z;
                         rn[3] += Jo[j].x * Jo[j].x; rn[4] += Jo[j].y * Jo[j].y; rn[5] += Jo[j].z * Jo[j].z;
-                        invD[j] = rcp_nr(fmaxf(dot3(Jp[j], Jp[j]) + dot3(Jo[j], Jo[j]), c.d_floor));
+                        invD[j] = rcp_nr(fmax(dot3(Jp[j], Jp[j]) + dot3(Jo[j], Jo[j]), T(c.d_floor)));
                     }
                 }
 #pragma unroll
-                for (int i = 0; i < 6; ++i) W[i] = (i < 3 ? c.w_p : c.w_o) * rcp_nr(1.f + sqrtf(rn[i]));
+                for (int i = 0; i < 6; ++i) W[i] = T(i < 3 ? c.w_p : c.w_o) * rcp_nr(T(1) + sqrt(rn[i]));
             }
-            const float c0 = cost_w(W, r.rho);
+            const T c0 = cost_w(W, r.rho);
             // ---- own LM trial at alpha = 1 (Alg. 4 l.3-9, first element of A)
             bool accepted = false;
             const bool have_lm = lm_direction<NMAX, EXACT>(rb, c, Jp, Jo, invD, W, r.rho, dth);
@@ -141,7 +141,7 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
 #pragma unroll
                 for (int j = 0; j < NMAX; ++j)
                     if (EXACT || j < n) tt[j] = clampf(th[j] + dth[j], rb.j[j].lo, rb.j[j].hi);
-                const Resid rt = eval_at<NMAX, EXACT>(rb, tg, tt);
+                const ResidT<T> rt = eval_at<NMAX, EXACT>(rb, tg, tt);
                 if (cost_w(W, rt.rho) < c0) {
                     accepted = true;
                     cnt[0]++;
@@ -151,7 +151,7 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
             }
             if (!accepted) {
                 // publish the rest of the cascade for the warp
-                float n0 = 0.f;
+                T n0 = T(0);
 #pragma unroll
                 for (int i = 0; i < 6; ++i) n0 += r.rho[i] * r.rho[i];
                 flags = have_lm ? 1 : 0;
@@ -212,29 +212,29 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
                 const int qq = it - (o > 0 ? S.incl[o - 1] : 0);   // item index within the owner's list
                 int kind, a;
                 decode_item(qq, S.flags[o], c.A, kind, a);
-                float alpha = 1.f;
-                for (int i = 0; i < a; ++i) alpha *= c.inv_beta;
-                float x[NMAX];
+                T alpha = T(1);
+                for (int i = 0; i < a; ++i) alpha *= T(c.inv_beta);
+                T x[NMAX];
 #pragma unroll
                 for (int j = 0; j < NMAX; ++j)
                     x[j] = (EXACT || j < n) ? clampf(S.th[j * nt + o] + alpha * S.dir[(kind * NMAX + j) * nt + o],
                                             rb.j[j].lo, rb.j[j].hi)
-                                   : 0.f;
-                const Resid rt = eval_at<NMAX, EXACT>(rb, tg, x);
+                                   : T(0);
+                const ResidT<T> rt = eval_at<NMAX, EXACT>(rb, tg, x);
                 bool ok;
                 if (kind == 1) {   // dogleg: unweighted |rho| (R23)
-                    float nt2 = 0.f;
+                    T nt2 = T(0);
 #pragma unroll
                     for (int i = 0; i < 6; ++i) nt2 += rt.rho[i] * rt.rho[i];
                     ok = nt2 < S.n0[o];
                 } else {           // Eq. 13 with W frozen at theta (R22)
-                    float s = 0.f;
+                    T s = T(0);
 #pragma unroll
                     for (int i = 0; i < 6; ++i) {
-                        const float wr = S.W[i * nt + o] * rt.rho[i];
+                        const T wr = S.W[i * nt + o] * rt.rho[i];
                         s += wr * wr;
                     }
-                    ok = 0.5f * s < S.c0[o];
+                    ok = T(0.5) * s < S.c0[o];
                 }
                 if (ok) atomicOr(&S.ok[o], 1ull << qq);
             }
@@ -245,15 +245,15 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
                     const int qq = __ffsll((long long)m) - 1;   // first success in cascade order
                     int kind, a;
                     decode_item(qq, flags, c.A, kind, a);
-                    float alpha = 1.f;
-                    for (int i = 0; i < a; ++i) alpha *= c.inv_beta;
+                    T alpha = T(1);
+                    for (int i = 0; i < a; ++i) alpha *= T(c.inv_beta);
 #pragma unroll
                     for (int j = 0; j < NMAX; ++j)
                         if (EXACT || j < n)
                             th[j] = clampf(th[j] + alpha * S.dir[(kind * NMAX + j) * nt + b], rb.j[j].lo, rb.j[j].hi);
                     cnt[kind]++;
                 } else {
-                    perturb<NMAX, EXACT>(rb, c, th, c.sigma_lm, tid, (uint32_t)b, P_PJPERT, (uint32_t)k);   // R25
+                    perturb<NMAX, EXACT>(rb, c, th, T(c.sigma_lm), tid, (uint32_t)b, P_PJPERT, (uint32_t)k);   // R25
                     cnt[3]++;
                 }
             }
@@ -273,21 +273,21 @@ k_pjik_coop(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg 
     if (iters_out) iters_out[row] = (c.target_early_exit || live) ? k : kseed;
 }
 
-template <int NMAX, bool EXACT>
-cudaError_t launch_coop_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
-                                 const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
-                                 int32_t* iters, cudaStream_t s) {
+template <class T, int NMAX, bool EXACT>
+cudaError_t launch_coop_t(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
+                          const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
+                          cudaStream_t s) {
     const int used = c.copies * c.K;
     const int block = (used + 31) / 32 * 32;
-    const size_t smem = coop_smem_bytes<NMAX>(block);
+    const size_t smem = coop_smem_bytes<T, NMAX>(block);
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pjik_coop<NMAX, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)coop_smem_bytes<NMAX>(256));
+        cudaError_t e = cudaFuncSetAttribute(k_pjik_coop<T, NMAX, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)coop_smem_bytes<T, NMAX>(256));
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_pjik_coop<NMAX, EXACT><<<T, block, smem, s>>>(rb, c, targets, seeds, theta, ep, eo, counts, iters);
+    k_pjik_coop<T, NMAX, EXACT><<<T_, block, smem, s>>>(rb, c, targets, seeds, theta, ep, eo, counts, iters);
     return cudaGetLastError();
 }
 

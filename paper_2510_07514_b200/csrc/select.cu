@@ -66,11 +66,14 @@ k_select_replicate(const __grid_constant__ DevRobot rb, const __grid_constant__ 
     }
 }
 
+// T = float (hjcd_solve) or double (hjcd_solve_f64: the ranking key keeps fp32
+// cost bits, the returned values are the fp64 ones)
+template <class T>
 __global__ void __launch_bounds__(128)
 k_select_best(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
-              const float* __restrict__ targets, const float* __restrict__ theta,
-              const float* __restrict__ ep_all, const float* __restrict__ eo_all,
-              float* __restrict__ q_out, float* __restrict__ pos_err, float* __restrict__ ori_err,
+              const float* __restrict__ targets, const T* __restrict__ theta,
+              const T* __restrict__ ep_all, const T* __restrict__ eo_all,
+              T* __restrict__ q_out, T* __restrict__ pos_err, T* __restrict__ ori_err,
               int32_t* __restrict__ status) {
     __shared__ unsigned long long red[32];
     const int t = blockIdx.x;
@@ -78,10 +81,10 @@ k_select_best(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCf
     const int used = c.copies * c.K;
     unsigned long long best = ~0ull;
     for (int b = threadIdx.x; b < used; b += blockDim.x) {
-        const float pe = ep_all[(long long)t * B + b], oe = eo_all[(long long)t * B + b];
-        const float cst = c.w_p * c.w_p * pe * pe + c.w_o * c.w_o * oe * oe;   // R14
+        const T pe = ep_all[(long long)t * B + b], oe = eo_all[(long long)t * B + b];
+        const float cst = (float)(T(c.w_p) * T(c.w_p) * pe * pe + T(c.w_o) * T(c.w_o) * oe * oe);   // R14
         // R27: converged seeds first (bit 63), then cost, then slot
-        const unsigned long long tier = (pe < c.eps_p_fine && oe < c.eps_o_fine) ? 0ull : 1ull;
+        const unsigned long long tier = (pe < T(c.eps_p_fine) && oe < T(c.eps_o_fine)) ? 0ull : 1ull;
         const unsigned long long key = (tier << 63) | ((unsigned long long)cost_bits(cst) << 32) | (unsigned)b;
         best = key < best ? key : best;
     }
@@ -111,16 +114,16 @@ k_select_best(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCf
     const bool valid = fabsf(nq - 1.f) <= 1e-3f && isfinite(nq) && isfinite(t7[0]) &&
                        isfinite(t7[1]) && isfinite(t7[2]);
     for (int j = threadIdx.x; j < n; j += blockDim.x)
-        q_out[(long long)t * n + j] = valid ? theta[((long long)t * B + bi) * n + j] : 0.f;
+        q_out[(long long)t * n + j] = valid ? theta[((long long)t * B + bi) * n + j] : T(0);
     if (threadIdx.x == 0) {
-        const float pe = valid ? ep_all[(long long)t * B + bi] : CUDART_INF_F;
-        const float oe = valid ? eo_all[(long long)t * B + bi] : CUDART_INF_F;
+        const T pe = valid ? ep_all[(long long)t * B + bi] : T(CUDART_INF_F);
+        const T oe = valid ? eo_all[(long long)t * B + bi] : T(CUDART_INF_F);
         pos_err[t] = pe;
         ori_err[t] = oe;
         int32_t s;
         if (!valid) s = HJCD_TARGET_INVALID;
-        else if (pe < c.eps_p_fine && oe < c.eps_o_fine) s = HJCD_TARGET_CONVERGED;
-        else if (pe < c.succ_p && oe < c.succ_o) s = HJCD_TARGET_SUCCESS;
+        else if (pe < T(c.eps_p_fine) && oe < T(c.eps_o_fine)) s = HJCD_TARGET_CONVERGED;
+        else if (pe < T(c.succ_p) && oe < T(c.succ_o)) s = HJCD_TARGET_SUCCESS;
         else s = HJCD_TARGET_NOT_CONVERGED;
         status[t] = s;
     }
@@ -175,13 +178,19 @@ cudaError_t launch_select_replicate(const DevRobot& rb, const DevCfg& c, const f
     return cudaGetLastError();
 }
 
-cudaError_t launch_select_best(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
-                               const float* theta, const float* ep_all, const float* eo_all,
-                               float* q_out, float* pos_err, float* ori_err, int32_t* status,
-                               cudaStream_t s) {
-    k_select_best<<<T, 128, 0, s>>>(rb, c, targets, theta, ep_all, eo_all, q_out, pos_err, ori_err, status);
+template <class T>
+cudaError_t launch_select_best(const DevRobot& rb, const DevCfg& c, const float* targets, int T_,
+                               const T* theta, const T* ep_all, const T* eo_all, T* q_out, T* pos_err,
+                               T* ori_err, int32_t* status, cudaStream_t s) {
+    k_select_best<T><<<T_, 128, 0, s>>>(rb, c, targets, theta, ep_all, eo_all, q_out, pos_err, ori_err, status);
     return cudaGetLastError();
 }
+template cudaError_t launch_select_best<float>(const DevRobot&, const DevCfg&, const float*, int, const float*,
+                                               const float*, const float*, float*, float*, float*, int32_t*,
+                                               cudaStream_t);
+template cudaError_t launch_select_best<double>(const DevRobot&, const DevCfg&, const float*, int, const double*,
+                                                const double*, const double*, double*, double*, double*, int32_t*,
+                                                cudaStream_t);
 
 cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, float* jac, cudaStream_t s) {
     const int block = 128;

@@ -25,7 +25,8 @@ EXPORTS = [
     "hjcd_robot_create", "hjcd_robot_extend", "hjcd_robot_destroy", "hjcd_robot_dof",
     "hjcd_robot_limits", "hjcd_config_default", "hjcd_workspace_size",
     "hjcd_workspace_size_host", "hjcd_solve", "hjcd_solve_timed", "hjcd_solve_host", "hjcd_ccd",
-    "hjcd_solve_batch", "hjcd_select_topn", "hjcd_mmd", "hjcd_fk", "hjcd_poccd",
+    "hjcd_solve_batch", "hjcd_select_topn", "hjcd_mmd", "hjcd_workspace_size_f64", "hjcd_solve_f64",
+    "hjcd_pjik_f64", "hjcd_fk", "hjcd_poccd",
     "hjcd_select_replicate", "hjcd_pjik", "hjcd_select_best", "hjcd_status_string",
     "hjcd_last_cuda_error", "hjcd_version",
 ]
@@ -86,6 +87,9 @@ def lib():
         L.hjcd_solve_batch.argtypes = [P, P, P, i32, i32, P, P, P, P, P, sz, P]
         L.hjcd_select_topn.argtypes = [P, P, P, i32, P, P, P, i32, P, P, P, P, P]
         L.hjcd_mmd.argtypes = [P, i32, P, i32, i32, i32, P, P, P]
+        L.hjcd_workspace_size_f64.argtypes = [P, i32, P, C.POINTER(sz)]
+        L.hjcd_solve_f64.argtypes = [P, P, P, i32, P, P, P, P, P, sz, P]
+        L.hjcd_pjik_f64.argtypes = [P, P, P, i32, P, P, P, P, P, P, P]
         L.hjcd_select_replicate.argtypes = [P, P, P, P, i32, P, P, P]
         L.hjcd_pjik.argtypes = [P, P, P, i32, P, P, P, P, P, P, P]
         L.hjcd_select_best.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P]
@@ -288,6 +292,46 @@ def solve_batch(robot: Robot, targets, N: int, cfg: Optional[hjcd_config] = None
     _check(lib().hjcd_solve_batch(robot.handle, C.byref(cfg), _ptr(targets), T, N, _ptr(q), _ptr(pe), _ptr(oe),
                                   _ptr(st), _ptr(ws), ws.numel(), _stream(stream)), "hjcd_solve_batch")
     return q, pe, oe, st
+
+
+def solve_f64(robot: Robot, targets, cfg: Optional[hjcd_config] = None, workspace: Optional[Workspace] = None,
+              stream=None):
+    """HJCD-IK with the fp64 polish (hjcd_solve_f64): fp32 targets [T, 7] ->
+    (q [T, dof] f64, pos_err [T] f64, ori_err [T] f64, status [T] int32)."""
+    torch = _torch()
+    cfg = cfg or default_config()
+    T = targets.shape[0]
+    _dev_f32(targets, (T, 7), "targets")
+    dev = targets.device
+    q = torch.empty((T, robot.dof), dtype=torch.float64, device=dev)
+    pe = torch.empty(T, dtype=torch.float64, device=dev)
+    oe = torch.empty(T, dtype=torch.float64, device=dev)
+    st = torch.empty(T, dtype=torch.int32, device=dev)
+    n = C.c_size_t()
+    _check(lib().hjcd_workspace_size_f64(robot.handle, T, C.byref(cfg), C.byref(n)), "hjcd_workspace_size_f64")
+    ws = _ws_for(dev, n.value, workspace)
+    _check(lib().hjcd_solve_f64(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(q), _ptr(pe), _ptr(oe), _ptr(st),
+                                _ptr(ws), ws.numel(), _stream(stream)), "hjcd_solve_f64")
+    return q, pe, oe, st
+
+
+def pjik_f64(robot: Robot, cfg: hjcd_config, targets, seeds, stream=None):
+    """Alg. 4 in fp64: fp32 seeds [T, B, n] -> dict theta [T, B, n], ep, eo [T, B]
+    (f64), counts [T, B, 4], iters [T, B]."""
+    torch = _torch()
+    T, n = targets.shape[0], robot.dof
+    _dev_f32(targets, (T, 7), "targets")
+    _dev_f32(seeds, (T, cfg.B, n), "seeds")
+    d = targets.device
+    out = dict(theta=torch.empty((T, cfg.B, n), dtype=torch.float64, device=d),
+               ep=torch.empty((T, cfg.B), dtype=torch.float64, device=d),
+               eo=torch.empty((T, cfg.B), dtype=torch.float64, device=d),
+               counts=torch.empty((T, cfg.B, 4), dtype=torch.int32, device=d),
+               iters=torch.empty((T, cfg.B), dtype=torch.int32, device=d))
+    _check(lib().hjcd_pjik_f64(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(seeds), _ptr(out["theta"]),
+                               _ptr(out["ep"]), _ptr(out["eo"]), _ptr(out["counts"]), _ptr(out["iters"]),
+                               _stream(stream)), "hjcd_pjik_f64")
+    return out
 
 
 def select_topn(robot: Robot, cfg: hjcd_config, targets, theta, ep, eo, N: int, stream=None):

@@ -310,6 +310,45 @@ def test_pjik_zero_error_fixed_point(hjcd_lib, cuda):
     assert np.array_equal(N(out["theta"]), seeds)
 
 
+# ---------------------------------------------------------------- fp64 polish (f1)
+@pytest.mark.parametrize("name,sigma,iters", [("panda", 0.05, 16), ("panda", 0.3, 64), ("fetch", 0.1, 32)])
+def test_pjik_f64_parity(hjcd_lib, cuda, name, sigma, iters):
+    # both sides fp64: only the operation order differs (push-through 6x6 vs the
+    # oracle's n x n solve, canonical frames vs 4x4 products), so clean seeds
+    # agree to ~1e-12, three orders of magnitude tighter than the fp32 bar
+    ch = inputs.robot(name)
+    Tn, B = 6, 40
+    p = params(B=B, K=10, lm_iters=iters, target_early_exit=0, eps_p_fine=1e-9, eps_o_fine=1e-8)
+    tg, th0 = targets_for(ch, Tn)
+    seeds = inputs.near_configs(ch, np.repeat(th0[:, None, :], B, 1), sigma, seed=8).astype(np.float32)
+    out = hjcd_lib.pjik_f64(hjcd_lib.Robot(ch), hjcd_lib.config_from_params(p), T(tg, cuda), T(seeds, cuda))
+    ref = oracle.pj_ik(ch, p, tg, seeds.astype(np.float64))
+    ep, eo = N(out["ep"]), N(out["eo"])
+    agree = (np.abs(ep - ref["ep"]) <= 1e-9) & (np.abs(eo - ref["eo"]) <= 1e-8)
+    clean = ref["margin"] >= 1e-6
+    assert not (clean & ~agree).any(), (clean & ~agree).sum()
+    assert agree.mean() >= 0.8, agree.mean()
+    # reported errors are those of the returned fp64 theta
+    th = N(out["theta"])
+    pose = oracle.fk(ch, th.reshape(-1, ch.dof)).reshape(Tn, B, 7)
+    ep64 = np.linalg.norm(pose[..., :3] - tg[:, None, :3].astype(np.float64), axis=-1)
+    assert np.abs(ep64 - ep).max() < 1e-12
+
+
+def test_solve_f64_reaches_spec_tolerances(hjcd_lib, cuda):
+    # SPEC's fine tolerances (1e-9 m / 1e-8 rad), reachable in fp64
+    ch = inputs.panda()
+    rb = hjcd_lib.Robot(ch)
+    tg, _ = targets_for(ch, 100)
+    p = params(eps_p_fine=1e-9, eps_o_fine=1e-8)
+    q, pe, oe, st = hjcd_lib.solve_f64(rb, T(tg, cuda), hjcd_lib.config_from_params(p))
+    q, pe, oe, st = N(q), N(pe), N(oe), N(st)
+    pe64, oe64 = fp64_errors(ch, q, tg)
+    assert np.abs(pe64 - pe).max() < 1e-12 and np.abs(oe64 - oe).max() < 1e-10
+    assert success(pe64, oe64).mean() >= 0.99
+    assert (st == 0).mean() >= 0.9 and np.median(pe64) < 1e-9, (np.mean(st == 0), np.median(pe64))
+
+
 # ---------------------------------------------------------------- solution batch + MMD (f2)
 def test_select_topn_and_solve_batch(hjcd_lib, cuda):
     ch = inputs.panda()
