@@ -216,10 +216,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; HJCD_DIST_BACKEND=gloo + more ranks than GPUs is a
+    # functional check of the multi-rank path on a single-GPU box (ranks share
+    # a device; the gather goes through host memory), not a scaling number
+    backend = os.environ.get("HJCD_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     rname, Tg, M, K, B, desc = CONFIGS[args.config]
     if args.targets:
@@ -270,7 +278,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ms_local = statistics.mean(step_ms)
     if world > 1:
-        t = torch.tensor([ms_local], device=dev)
+        t = torch.tensor([ms_local], device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     else:
@@ -388,7 +396,7 @@ def main():
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
     e2e_local = statistics.mean(e2e_ms)
     if world > 1:
-        t = torch.tensor([e2e_local], device=dev)
+        t = torch.tensor([e2e_local], device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_local = float(t.item())
     e2e = {"value": total_targets / (e2e_local / 1e3), "unit": UNIT, "h2d_bytes_per_step": Tg * 7 * 4,
@@ -405,7 +413,8 @@ def main():
                "config": {"workload": f"{args.config}: {desc}", "robot": rname, "targets_per_gpu": Tg,
                           "global_targets": total_targets, "M": M, "K": K, "B": B, "ccd_iters": cfg.ccd_iters,
                           "lm_iters": cfg.lm_iters, "parallelism": f"targets partitioned over {world} GPU(s)"
-                          + (" + NCCL all_gather of results" if world > 1 else ""),
+                          + ((" + NCCL all_gather of results" if backend == "nccl" else
+                                      f" + {backend} all_gather (functional check, ranks share a GPU)") if world > 1 else ""),
                           "l2": "flushed between steps (256 MiB write)"},
                "p50_ms": srt[len(srt) // 2], "p99_ms": srt[min(len(srt) - 1, int(math.ceil(0.99 * len(srt))) - 1)],
                "latency_note": "p50/p99 of the per-step batch latency (one hjcd_solve of all targets)",

@@ -42,6 +42,10 @@ def _all_gather_rows(rows: torch.Tensor, group=None) -> torch.Tensor:
     out = torch.empty((world * rows.shape[0], rows.shape[1]), dtype=rows.dtype, device=rows.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, rows, group=group)
+    elif rows.is_cuda:   # gloo with device tensors (functional multi-rank check): via host memory
+        host = [torch.empty_like(rows, device="cpu") for _ in range(world)]
+        dist.all_gather(host, rows.cpu(), group=group)
+        out.copy_(torch.cat(host))
     else:
         dist.all_gather(list(out.chunk(world)), rows, group=group)
     return out
