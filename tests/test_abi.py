@@ -110,3 +110,35 @@ def test_oracle_and_cuda_path_share_nothing():
         assert "import oracle" not in txt and "from oracle" not in txt, f
     otxt = open(os.path.join(ROOT, "oracle", "hjcd_oracle.cpp")).read()
     assert "#include \"" not in otxt
+
+
+def test_new_entry_points_validate_before_cuda(hjcd_lib):
+    # argument errors are synchronous status returns, before any CUDA call
+    L = hjcd_lib.lib()
+    r = hjcd_lib.Robot.panda()
+    c = hjcd_lib.default_config()
+    fake = C.c_void_p(256)
+    # solution batch: N must be in 1..floor(B/K)*K
+    for N in (0, 101):
+        assert L.hjcd_solve_batch(r.handle, C.byref(c), fake, 4, N, fake, fake, fake, fake, fake, 1 << 40,
+                                  None) == 1
+        assert L.hjcd_select_topn(r.handle, C.byref(c), fake, 4, fake, fake, fake, N, fake, fake, fake, None,
+                                  None) == 1
+    # MMD: N + N2 <= 256, dim 1..32
+    assert L.hjcd_mmd(fake, 200, fake, 100, 7, 3, fake, None, None) == 2
+    assert L.hjcd_mmd(fake, 10, fake, 10, 33, 3, fake, None, None) == 1
+    assert L.hjcd_mmd(None, 10, fake, 10, 7, 3, fake, None, None) == 1
+    # fp64 workspace is larger than the fp32 one (fp64 theta / errors)
+    n32, n64 = C.c_size_t(), C.c_size_t()
+    assert L.hjcd_workspace_size(r.handle, 1000, C.byref(c), C.byref(n32)) == 0
+    assert L.hjcd_workspace_size_f64(r.handle, 1000, C.byref(c), C.byref(n64)) == 0
+    assert n64.value > n32.value and n64.value % 256 == 0
+    assert L.hjcd_solve_f64(r.handle, C.byref(c), fake, 10, fake, fake, fake, fake, fake, 1024, None) == 4
+    # classic CCD / stage calls reject null outputs
+    assert L.hjcd_ccd(r.handle, C.byref(c), fake, 4, None, None, None, None, None) == 1
+    assert L.hjcd_pjik_f64(r.handle, C.byref(c), fake, 4, None, fake, fake, fake, None, None, None) == 1
+    # the PO-CCD stop rule needs one cluster per target: M <= 2048
+    big = hjcd_lib.default_config(M=3000)
+    assert L.hjcd_poccd(r.handle, C.byref(big), fake, 1, None, fake, fake, None, None, None, None) == 2
+    ok = hjcd_lib.default_config(M=3000, ccd_early_exit=0)
+    assert L.hjcd_workspace_size(r.handle, 10, C.byref(ok), C.byref(n32)) == 0
