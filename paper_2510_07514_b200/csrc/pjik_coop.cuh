@@ -62,6 +62,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
             int32_t* __restrict__ counts_out, int32_t* __restrict__ iters_out) {
     extern __shared__ unsigned long long coop_raw[];
     __shared__ int s_wtot[8];   // per-warp item totals (<= 256 threads)
+    __shared__ T s_alpha[32];   // line-search steps beta^-a, a = 0..A (A <= 31), by repeated products
     const int nt = blockDim.x;
     const CoopSmem<T> S = coop_smem<T, NMAX>(coop_raw, nt);
     const int n = rb.n;
@@ -73,6 +74,10 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
     const TargetT<T> tg = load_target<T>(targets + 7ll * t);
     const uint32_t tid = (uint32_t)(c.tid_offset + t);
     const long long row = (long long)t * c.B + b;
+    if (b == 0) {
+        T al = T(1);
+        for (int a = 0; a < 32; ++a) { s_alpha[a] = al; al *= T(c.inv_beta); }
+    }   // published by the first __syncthreads_or of the iteration loop
 
     T th[NMAX], tt[NMAX], dth[NMAX];
 #pragma unroll
@@ -212,8 +217,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                 const int qq = it - (o > 0 ? S.incl[o - 1] : 0);   // item index within the owner's list
                 int kind, a;
                 decode_item(qq, S.flags[o], c.A, kind, a);
-                T alpha = T(1);
-                for (int i = 0; i < a; ++i) alpha *= T(c.inv_beta);
+                const T alpha = s_alpha[a];
                 T x[NMAX];
 #pragma unroll
                 for (int j = 0; j < NMAX; ++j)
@@ -245,8 +249,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                     const int qq = __ffsll((long long)m) - 1;   // first success in cascade order
                     int kind, a;
                     decode_item(qq, flags, c.A, kind, a);
-                    T alpha = T(1);
-                    for (int i = 0; i < a; ++i) alpha *= T(c.inv_beta);
+                    const T alpha = s_alpha[a];
 #pragma unroll
                     for (int j = 0; j < NMAX; ++j)
                         if (EXACT || j < n)
