@@ -29,7 +29,8 @@ struct CoopSmem {
     T* c0;         // [nt]
     T* n0;         // [nt]
     int* flags;    // [nt]  bit0 LM, bit1 dogleg, bit2 single
-    int* incl;     // [nt]  inclusive prefix of pending items within the CTA
+    unsigned char* own;    // [64 nt]  pending item -> owner slot
+    unsigned char* ownq;   // [64 nt]  pending item -> index in the owner's cascade
     unsigned long long* ok;   // [nt]  success bits in cascade order
 };
 
@@ -45,13 +46,14 @@ __device__ __forceinline__ CoopSmem<T> coop_smem(void* base, int nt) {
     s.c0 = f; f += nt;
     s.n0 = f; f += nt;
     s.flags = (int*)f;
-    s.incl = s.flags + nt;
+    s.own = (unsigned char*)(s.flags + nt);
+    s.ownq = s.own + 64 * nt;
     return s;
 }
 
 template <class T, int NMAX>
 size_t coop_smem_bytes(int nt) {
-    return (size_t)nt * (8 + sizeof(T) * (4 * NMAX + 6 + 2) + 4 * 2);
+    return (size_t)nt * (8 + sizeof(T) * (4 * NMAX + 6 + 2) + 4 + 2 * 64);
 }
 
 template <class T, int NMAX, bool EXACT>
@@ -204,17 +206,15 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
             total += v;
         }
         if (total > 0) {   // uniform over the CTA
-            S.incl[b] = incl;
+            // item -> (owner, index) table: each failing seed fills its range
+            for (int i = 0; i < items; ++i) {
+                S.own[incl - items + i] = (unsigned char)b;
+                S.ownq[incl - items + i] = (unsigned char)i;
+            }
             __syncthreads();
             for (int it = b; it < total; it += nt) {
-                // owner = first slot whose inclusive prefix exceeds it
-                int lo = 0, hi = nt - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (S.incl[mid] > it) hi = mid; else lo = mid + 1;
-                }
-                const int o = lo;
-                const int qq = it - (o > 0 ? S.incl[o - 1] : 0);   // item index within the owner's list
+                const int o = S.own[it];
+                const int qq = S.ownq[it];   // item index within the owner's list
                 int kind, a;
                 decode_item(qq, S.flags[o], c.A, kind, a);
                 const T alpha = s_alpha[a];
