@@ -110,8 +110,9 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
         }
         if (k == c.lm_iters) break;
 
-        bool need = false;
+        bool need = false, have_lm = false, accepted = false;
         int flags = 0, items = 0;
+        T W[6], c0 = T(0);
         if (live) {
             // ---- Eq. 7 Jacobian, W (R17), D (R20), c_W(theta), |rho|^2
 #pragma unroll
@@ -126,7 +127,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                     }
                 }
             }
-            T W[6], invD[NMAX];
+            T invD[NMAX];
             {
                 T rn[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
 #pragma unroll
@@ -140,90 +141,93 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
 #pragma unroll
                 for (int i = 0; i < 6; ++i) W[i] = T(i < 3 ? c.w_p : c.w_o) * rcp_nr(T(1) + sqrt(rn[i]));
             }
-            const T c0 = cost_w(W, r.rho);
-            // ---- own LM trial at alpha = 1 (Alg. 4 l.3-9, first element of A)
-            bool accepted = false;
-            const bool have_lm = lm_direction<NMAX, EXACT>(rb, c, Jp, Jo, invD, W, r.rho, dth);
-            if (have_lm) {
-#pragma unroll
-                for (int j = 0; j < NMAX; ++j)
-                    if (EXACT || j < n) tt[j] = clampf(th[j] + dth[j], rb.j[j].lo, rb.j[j].hi);
-                const ResidT<T> rt = eval_at<NMAX, EXACT>(rb, tg, tt);
-                if (cost_w(W, rt.rho) < c0) {
-                    accepted = true;
-                    cnt[0]++;
-#pragma unroll
-                    for (int j = 0; j < NMAX; ++j) th[j] = tt[j];
-                }
-            }
-            if (!accepted) {
-                // publish the rest of the cascade for the warp
-                T n0 = T(0);
-#pragma unroll
-                for (int i = 0; i < 6; ++i) n0 += r.rho[i] * r.rho[i];
-                flags = have_lm ? 1 : 0;
-#pragma unroll
-                for (int j = 0; j < NMAX; ++j) {
-                    S.th[j * nt + b] = th[j];
-                    S.dir[(0 * NMAX + j) * nt + b] = dth[j];
-                }
-                if (dogleg_direction<NMAX, EXACT>(rb, c, Jp, Jo, r.rho, dth, tt)) {
-                    flags |= 2;
-#pragma unroll
-                    for (int j = 0; j < NMAX; ++j) S.dir[(1 * NMAX + j) * nt + b] = dth[j];
-                }
-                if (single_coord_direction<NMAX, EXACT>(rb, c, Jp, Jo, W, r.rho, dth)) {
-                    flags |= 4;
-#pragma unroll
-                    for (int j = 0; j < NMAX; ++j) S.dir[(2 * NMAX + j) * nt + b] = dth[j];
-                }
-#pragma unroll
-                for (int i = 0; i < 6; ++i) S.W[i * nt + b] = W[i];
-                S.c0[b] = c0;
-                S.n0[b] = n0;
-                S.flags[b] = flags;
-                items = ((flags & 1) ? c.A : 0) + ((flags & 2) ? 1 : 0) + ((flags & 4) ? c.A + 1 : 0);
-                need = true;
-            }
+            c0 = cost_w(W, r.rho);
+            have_lm = lm_direction<NMAX, EXACT>(rb, c, Jp, Jo, invD, W, r.rho, dth);
         }
 
-        // ---- CTA-cooperative evaluation of the pending cascade trials (K6):
-        // the items of every failing seed of the target are spread over all
-        // the CTA's lanes (the iteration lasts as long as its slowest warp)
-        int incl = items;
+        // ---- trial evaluation, ONE site in two phases (K6).  Phase 0: every
+        // live seed evaluates its own LM trial at alpha = 1 (Alg. 4 l.3-9, the
+        // common case).  Phase 1, CTA-cooperative: the seeds whose alpha = 1
+        // trial failed publish theta, their three directions, W, c0 and |rho|^2;
+        // the rest of their cascades (LM alpha_1..alpha_A, dogleg, single
+        // alpha_0..alpha_A) is spread over all the CTA's lanes, and each takes
+        // the FIRST success in cascade order.
+        const bool pending = live && have_lm;
+        for (int phase = 0; phase < 2; ++phase) {
+            int total = 0;
+            if (phase == 1) {
+                need = live && !accepted;
+                if (need) {
+                    T n0 = T(0);
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= off) incl += v;
-        }
-        if (lane == 31) s_wtot[b >> 5] = incl;
-        S.ok[b] = 0ull;
-        __syncthreads();
-        int total = 0;
-        for (int w = 0; w < (nt >> 5); ++w) {
-            const int v = s_wtot[w];
-            if (w < (b >> 5)) incl += v;
-            total += v;
-        }
-        if (total > 0) {   // uniform over the CTA
-            // item -> (owner, index) table: each failing seed fills its range
-            for (int i = 0; i < items; ++i) {
-                S.own[incl - items + i] = (unsigned char)b;
-                S.ownq[incl - items + i] = (unsigned char)i;
+                    for (int i = 0; i < 6; ++i) n0 += r.rho[i] * r.rho[i];
+                    flags = have_lm ? 1 : 0;
+#pragma unroll
+                    for (int j = 0; j < NMAX; ++j) {
+                        S.th[j * nt + b] = th[j];
+                        S.dir[(0 * NMAX + j) * nt + b] = dth[j];
+                    }
+                    if (dogleg_direction<NMAX, EXACT>(rb, c, Jp, Jo, r.rho, dth, tt)) {   // Eqs. 14-15
+                        flags |= 2;
+#pragma unroll
+                        for (int j = 0; j < NMAX; ++j) S.dir[(1 * NMAX + j) * nt + b] = dth[j];
+                    }
+                    if (single_coord_direction<NMAX, EXACT>(rb, c, Jp, Jo, W, r.rho, dth)) {   // Eq. 16
+                        flags |= 4;
+#pragma unroll
+                        for (int j = 0; j < NMAX; ++j) S.dir[(2 * NMAX + j) * nt + b] = dth[j];
+                    }
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) S.W[i * nt + b] = W[i];
+                    S.c0[b] = c0;
+                    S.n0[b] = n0;
+                    S.flags[b] = flags;
+                    items = ((flags & 1) ? c.A : 0) + ((flags & 2) ? 1 : 0) + ((flags & 4) ? c.A + 1 : 0);
+                }
+                int incl = items;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= off) incl += v;
+                }
+                if (lane == 31) s_wtot[b >> 5] = incl;
+                S.ok[b] = 0ull;
+                __syncthreads();
+                for (int w = 0; w < (nt >> 5); ++w) {
+                    const int v = s_wtot[w];
+                    if (w < (b >> 5)) incl += v;
+                    total += v;
+                }
+                if (total == 0) break;   // uniform over the CTA
+                // item -> (owner, index) table: each failing seed fills its range
+                for (int i = 0; i < items; ++i) {
+                    S.own[incl - items + i] = (unsigned char)b;
+                    S.ownq[incl - items + i] = (unsigned char)i;
+                }
+                __syncthreads();
             }
-            __syncthreads();
-            for (int it = b; it < total; it += nt) {
-                const int o = S.own[it];
-                const int qq = S.ownq[it];   // item index within the owner's list
-                int kind, a;
-                decode_item(qq, S.flags[o], c.A, kind, a);
-                const T alpha = s_alpha[a];
+            bool own_ok = false;
+            for (int it = b;; it += nt) {
+                int o = b, qq = 0, kind = 0, a = 0;
                 T x[NMAX];
+                if (phase == 0) {
+                    if (it != b || !pending) break;
 #pragma unroll
-                for (int j = 0; j < NMAX; ++j)
-                    x[j] = (EXACT || j < n) ? clampf(S.th[j * nt + o] + alpha * S.dir[(kind * NMAX + j) * nt + o],
-                                            rb.j[j].lo, rb.j[j].hi)
+                    for (int j = 0; j < NMAX; ++j)
+                        x[j] = (EXACT || j < n) ? clampf(th[j] + dth[j], rb.j[j].lo, rb.j[j].hi) : T(0);
+                } else {
+                    if (it >= total) break;
+                    o = S.own[it];
+                    qq = S.ownq[it];   // item index within the owner's list
+                    decode_item(qq, S.flags[o], c.A, kind, a);
+                    const T alpha = s_alpha[a];
+#pragma unroll
+                    for (int j = 0; j < NMAX; ++j)
+                        x[j] = (EXACT || j < n)
+                                   ? clampf(S.th[j * nt + o] + alpha * S.dir[(kind * NMAX + j) * nt + o], rb.j[j].lo,
+                                            rb.j[j].hi)
                                    : T(0);
+                }
                 const ResidT<T> rt = eval_at<NMAX, EXACT>(rb, tg, x);
                 bool ok;
                 if (kind == 1) {   // dogleg: unweighted |rho| (R23)
@@ -232,15 +236,32 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                     for (int i = 0; i < 6; ++i) nt2 += rt.rho[i] * rt.rho[i];
                     ok = nt2 < S.n0[o];
                 } else {           // Eq. 13 with W frozen at theta (R22)
-                    T s = T(0);
+                    T sw = T(0);
 #pragma unroll
                     for (int i = 0; i < 6; ++i) {
-                        const T wr = S.W[i * nt + o] * rt.rho[i];
-                        s += wr * wr;
+                        const T wr = (phase == 0 ? W[i] : S.W[i * nt + o]) * rt.rho[i];
+                        sw += wr * wr;
                     }
-                    ok = T(0.5) * s < S.c0[o];
+                    ok = T(0.5) * sw < (phase == 0 ? c0 : S.c0[o]);
                 }
-                if (ok) atomicOr(&S.ok[o], 1ull << qq);
+                if (phase == 0) {
+                    own_ok = ok;
+                    if (ok) {   // the LM step at alpha = 1 is accepted
+#pragma unroll
+                        for (int j = 0; j < NMAX; ++j) tt[j] = x[j];
+                    }
+                } else if (ok) {
+                    atomicOr(&S.ok[o], 1ull << qq);
+                }
+            }
+            if (phase == 0) {
+                if (own_ok) {
+                    accepted = true;
+                    cnt[0]++;
+#pragma unroll
+                    for (int j = 0; j < NMAX; ++j) th[j] = tt[j];
+                }
+                continue;
             }
             __syncthreads();
             if (need) {
@@ -256,7 +277,8 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                             th[j] = clampf(th[j] + alpha * S.dir[(kind * NMAX + j) * nt + b], rb.j[j].lo, rb.j[j].hi);
                     cnt[kind]++;
                 } else {
-                    perturb<NMAX, EXACT>(rb, c, th, T(c.sigma_lm), tid, (uint32_t)b, P_PJPERT, (uint32_t)k);   // R25
+                    // R25; SFU Box-Muller in fp32 (K5: ~1e-6 relative on a sigma = 0.05 kick)
+                    perturb<NMAX, EXACT, true>(rb, c, th, T(c.sigma_lm), tid, (uint32_t)b, P_PJPERT, (uint32_t)k);
                     cnt[3]++;
                 }
             }
