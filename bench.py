@@ -306,16 +306,20 @@ def main():
     poccd_flops = iters_sum * flops_poccd_iter(n) + seeds_total * flops_poccd_final(n)
     pjik_flops = pj_iters_sum * flops_pjik_iter(n)
     ach = poccd_flops / (kmean["k_poccd"] / 1e3) / 1e12
-    traffic = None
+    traffic, exec_flops = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(args.config, {}).get("k_poccd")
+            tj = json.load(f)
+        traffic = tj.get(args.config, {}).get("k_poccd")
+        exec_flops = tj.get("_executed_fp32_flops", {}).get(args.config, {}).get("k_poccd")
     except Exception:
         pass
     roofline = {"bound": "alu", "kernel": "k_poccd", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": ach / peak_tf, "traffic": traffic,
                 "peak_source": f"148 SM x 128 FP32 lanes x 2 x {mhz:.0f} MHz ({peak_src})",
                 "algorithmic_flops_per_launch": poccd_flops,
+                "ncu_executed_fp32_flops_per_launch": exec_flops,
+                "ncu_executed_frac": (exec_flops / (kmean["k_poccd"] / 1e3) / 1e12 / peak_tf) if exec_flops else None,
                 "unit_flops": f"{flops_poccd_iter(n)} per seed-iteration + {flops_poccd_final(n)} per seed",
                 "kernel_ms": kmean, "kernel_ms_source": "library events at the stage boundaries of every timed step",
                 "share_of_step": {k: v / sum(kmean.values()) for k, v in kmean.items()},

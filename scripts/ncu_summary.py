@@ -87,10 +87,12 @@ def opcode_mix(rep, kernel_regex):
         if hdr and len(r) == len(hdr):
             body.append(r)
     if not hdr:
-        return {}, {}
+        return {}, {}, {}
     ie, src = hdr.index("Instructions Executed"), hdr.index("Source")
+    ti = hdr.index("Predicated-On Thread Instructions Executed") if "Predicated-On Thread Instructions Executed" in hdr else None
     st = hdr.index("Warp Stall Sampling (All Samples)") if "Warp Stall Sampling (All Samples)" in hdr else None
     ops, stalls = collections.Counter(), collections.Counter()
+    thread_ops = collections.Counter()
     for r in body:
         toks = r[src].strip().split()
         if not toks:
@@ -98,9 +100,11 @@ def opcode_mix(rep, kernel_regex):
         op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
         op = op.split(".")[0]
         ops[op] += int(_num(r[ie]) or 0)
+        if ti is not None:
+            thread_ops[op] += int(_num(r[ti]) or 0)
         if st is not None:
             stalls[op] += int(_num(r[st]) or 0)
-    return ops, stalls
+    return ops, stalls, thread_ops
 
 
 def main():
@@ -141,8 +145,18 @@ def main():
             lines += ["", "Top stall reasons (sampled):", ""]
             lines += [f"- `{k}`: {v}" for k, v in top]
         base = short.split("<")[0]
-        ops, stalls = opcode_mix(rep, base)
+        ops, stalls, tops = opcode_mix(rep, base)
         tot = sum(ops.values())
+        if tops:
+            # executed FP32 flops from the per-instruction predicated-on thread counts
+            fl = 2 * tops.get("FFMA", 0) + tops.get("FMUL", 0) + tops.get("FADD", 0)
+            dur = d.get("gpu__time_duration.sum", ("", ""))
+            dur_s = _num(dur[0]) * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(
+                dur[1], 1e-3) if _num(dur[0]) else None
+            lines += ["", f"Executed FP32 flops per launch (2 FFMA + FMUL + FADD, thread level): {fl:.4g}"]
+            if dur_s:
+                lines.append(f"Executed FP32 rate: {fl / dur_s / 1e12:.2f} TFLOP/s at the captured duration")
+                traffic.setdefault("_executed_fp32_flops", {}).setdefault(config, {})[base] = fl
         if tot:
             lines += ["", f"SASS opcode mix (warp-level executed instructions, total {tot}):", "",
                       "| opcode | share | stall samples |", "|---|---|---|"]
