@@ -512,6 +512,32 @@ def test_edge_cases(hjcd_lib, cuda):
     assert N(st)[0] == 0 and np.abs(N(q)[0] - [0.7, -1.1]).max() < 1e-3
 
 
+def test_maximum_sizes(hjcd_lib, cuda):
+    # the limits the ABI documents: n = 32 DoF, M = 2048 in one 16-CTA cluster
+    # (stop rule), B = 256 polish seeds in one CTA, M = 8192 (per-seed stage 1,
+    # 64 KB bitonic top-K); results stay valid and within limits
+    ch = inputs.robot("panda_x32")
+    rb = hjcd_lib.Robot(ch)
+    tg, _ = targets_for(ch, 4)
+    p = params(M=2048, K=32, B=256, lm_iters=64)
+    q, pe, oe, st = [N(x) for x in hjcd_lib.solve(rb, T(tg, cuda), hjcd_lib.config_from_params(p))]
+    pe64, oe64 = fp64_errors(ch, q, tg)
+    assert np.abs(pe64 - pe).max() < 5e-6 and success(pe64, oe64).all()
+    lo, hi = [x.astype(np.float32) for x in ch.limits()]
+    assert np.all(q >= lo) and np.all(q <= hi)
+    ch7 = inputs.panda()
+    rb7 = hjcd_lib.Robot(ch7)
+    tg7, _ = targets_for(ch7, 3)
+    p = params(M=8192, K=64, B=128, ccd_early_exit=0, ccd_iters=16)
+    q, pe, oe, st = [N(x) for x in hjcd_lib.solve(rb7, T(tg7, cuda), hjcd_lib.config_from_params(p))]
+    assert success(*fp64_errors(ch7, q, tg7)).all()
+    # beyond the limits: clean status errors, no launch
+    with pytest.raises(hjcd_lib.HjcdError, match="unsupported"):
+        hjcd_lib.solve(rb7, T(tg7, cuda), hjcd_lib.config_from_params(params(M=2049)))
+    with pytest.raises(hjcd_lib.HjcdError, match="unsupported"):
+        hjcd_lib.solve(rb7, T(tg7, cuda), hjcd_lib.config_from_params(params(K=50, B=300)))
+
+
 @pytest.mark.parametrize("name", ["fetch", "panda_x14", "panda_x24"])
 def test_solve_other_chains(hjcd_lib, cuda, name):
     ch = inputs.robot(name)
