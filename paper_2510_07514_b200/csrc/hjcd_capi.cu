@@ -164,6 +164,7 @@ hjcd_status build_robot(const hjcd_joint* joints, int32_t num, const double ee_x
         dd.lo = (double)dj.lo;
         dd.hi = (double)dj.hi;
         dd.type = j.type;
+        if (j.type == HJCD_PRISMATIC) { r->dev.pmask |= 1u << d; r->dev64.pmask |= 1u << d; }
         acc = rt_transpose_rot(C);
         d++;
     }

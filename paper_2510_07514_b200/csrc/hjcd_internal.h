@@ -29,7 +29,8 @@ struct DevJointT {
 template <class S>
 struct DevRobotT {
     int32_t n;
-    int32_t pad[3];
+    uint32_t pmask;      // bit j set: DoF joint j is prismatic
+    int32_t pad[2];
     DevJointT<S> j[HJCD_MAX_DOF];
     S eeR[9];
     S eet[3];

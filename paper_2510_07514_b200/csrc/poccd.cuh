@@ -43,6 +43,10 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     int t, m;
     bool active = true;
     __shared__ int s_flag[3];
+    // the frames (P_j, z_j) of this iteration, per thread, so the two moved
+    // joints' frames are two indexed loads instead of 2 x NMAX predicated selects
+    constexpr bool FRAMES_SMEM = NMAX <= 16;
+    extern __shared__ float4 s_frames[];   // [NMAX][blockDim] (P.xyz, z.x), then float2 [NMAX][blockDim] (z.yz)
     if (TEXIT) {
         t = (int)(blockIdx.x / (unsigned)CL);
         m = (int)(blockIdx.x - (unsigned)t * CL) * (int)blockDim.x + (int)threadIdx.x;
@@ -90,6 +94,16 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     int k;
     for (k = 0;; ++k, rho_k *= c.delta_rho) {
         fk<NMAX, true, EXACT, true>(rb, th, P, Z, pe, qe);
+        if constexpr (FRAMES_SMEM) {
+            float2* s_fz = (float2*)(s_frames + NMAX * blockDim.x);
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j) {
+                if (EXACT || j < n) {
+                    s_frames[j * blockDim.x + threadIdx.x] = make_float4(P[j].x, P[j].y, P[j].z, Z[j].x);
+                    s_fz[j * blockDim.x + threadIdx.x] = make_float2(Z[j].y, Z[j].z);
+                }
+            }
+        }
         const float3 rp = tg.p - pe;                   // r_p (Eq. 4)
         const Quat qr = quat_err(tg.q, qe);            // q_err (Eq. 5), w >= 0
         const float sv = sqrtf(qr.x * qr.x + qr.y * qr.y + qr.z * qr.z);
@@ -201,12 +215,25 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         // frames of the two moved joints (uniform-index selects, no local memory);
         // an orientation winner is always revolute (prismatic candidates are 0)
         float3 Pa = f3(0.f, 0.f, 0.f), Za = Pa, Pb = Pa, Zb = Pa;
-        int ta = HJCD_REVOLUTE, tb = HJCD_REVOLUTE;
+        const int ta = (ja >= 0 && ((rb.pmask >> ja) & 1u)) ? HJCD_PRISMATIC : HJCD_REVOLUTE;
+        const int tb = ((rb.pmask >> jb) & 1u) ? HJCD_PRISMATIC : HJCD_REVOLUTE;
+        if constexpr (FRAMES_SMEM) {
+            const float2* s_fz = (const float2*)(s_frames + NMAX * blockDim.x);
+            const float4 fb = s_frames[jb * blockDim.x + threadIdx.x];
+            const float2 gb = s_fz[jb * blockDim.x + threadIdx.x];
+            Pb = f3(fb.x, fb.y, fb.z); Zb = f3(fb.w, gb.x, gb.y);
+            if (ja >= 0) {
+                const float4 fa = s_frames[ja * blockDim.x + threadIdx.x];
+                const float2 ga = s_fz[ja * blockDim.x + threadIdx.x];
+                Pa = f3(fa.x, fa.y, fa.z); Za = f3(fa.w, ga.x, ga.y);
+            }
+        } else {
 #pragma unroll
-        for (int j = 0; j < NMAX; ++j) {
-            if (EXACT || j < n) {
-                if (j == ja) { Pa = P[j]; Za = Z[j]; ta = rb.j[j].type; }
-                if (j == jb) { Pb = P[j]; Zb = Z[j]; tb = rb.j[j].type; }
+            for (int j = 0; j < NMAX; ++j) {
+                if (EXACT || j < n) {
+                    if (j == ja) { Pa = P[j]; Za = Z[j]; }
+                    if (j == jb) { Pb = P[j]; Zb = Z[j]; }
+                }
             }
         }
         // r(theta_hat) exactly: downstream joint's rigid motion first, then the
@@ -266,6 +293,11 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     if (iters_out) iters_out[o] = k;
 }
 
+template <int NMAX>
+inline size_t poccd_smem(int nt) {   // the per-thread frames (24 B per joint) for NMAX <= 16
+    return NMAX <= 16 ? (size_t)NMAX * nt * (sizeof(float4) + sizeof(float2)) : 0;
+}
+
 // seeds per CTA (nt) and CTAs per cluster (CL) of the lockstep launch:
 // 128-thread CTAs (32 for M < 128), up to 16 per cluster (non-portable size
 // above 8), so M <= 2048
@@ -283,8 +315,8 @@ cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* tar
         const int block = 128;
         const long long grid = (total + block - 1) / block;
         if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-        k_poccd<NMAX, EXACT, false><<<(unsigned)grid, block, 0, s>>>(rb, c, targets, T, seeds, theta, cost, ep, eo,
-                                                                      iters, 1);
+        k_poccd<NMAX, EXACT, false><<<(unsigned)grid, block, poccd_smem<NMAX>(block), s>>>(
+            rb, c, targets, T, seeds, theta, cost, ep, eo, iters, 1);
         return cudaGetLastError();
     }
     int nt, CL;
@@ -304,7 +336,7 @@ cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* tar
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid, 1, 1);
     cfg.blockDim = dim3(nt, 1, 1);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = poccd_smem<NMAX>(nt);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
