@@ -149,7 +149,8 @@ __device__ __forceinline__ void sincos_b(double x, double* s, double* c) { sinco
 // EXACT: the chain has exactly NMAX DoF (no per-joint guard).  FAST: joint
 // sincos on the SFU (__sincosf, |err| <~ 5e-7 rad on the joint ranges): used by
 // the coarse stage only (K5); the polish stage uses sincos_b.
-template <int NMAX, bool FRAMES, bool EXACT = false, bool FAST = false, class T>
+// REV: every DoF joint is revolute (no per-joint type branch).
+template <int NMAX, bool FRAMES, bool EXACT = false, bool FAST = false, bool REV = false, class T>
 __device__ __forceinline__ void fk(const DevRobotT<T>& rb, const T (&th)[NMAX], vec3<T> (&P)[NMAX],
                                    vec3<T> (&Z)[NMAX], vec3<T>& pe, QuatT<T>& qe) {
     T R[9] = {T(1), T(0), T(0), T(0), T(1), T(0), T(0), T(0), T(1)};
@@ -171,7 +172,7 @@ __device__ __forceinline__ void fk(const DevRobotT<T>& rb, const T (&th)[NMAX], 
                 P[j] = mk3<T>(tx, ty, tz);
                 Z[j] = mk3<T>(N[2], N[5], N[8]);
             }
-            if (J.type == HJCD_REVOLUTE) {
+            if (REV || J.type == HJCD_REVOLUTE) {
                 T s, c;
                 if constexpr (FAST) __sincosf(th[j], &s, &c);
                 else sincos_b(th[j], &s, &c);

@@ -29,10 +29,11 @@ namespace hjcd {
 //   "converged" votes into a 3-slot flag ring in each CTA's shared memory
 //   (DSMEM stores, then barrier.cluster arrive.release / wait.acquire); all
 //   seeds of the target stop at the first iteration in which any seed passed.
-template <int NMAX, bool EXACT, bool TEXIT>
+// REV: every DoF joint is revolute (no per-joint type branches).
 #ifndef HJCD_POCCD_MINB
 #define HJCD_POCCD_MINB 4
 #endif
+template <int NMAX, bool EXACT, bool TEXIT, bool REV>
 __global__ void __launch_bounds__(128, HJCD_POCCD_MINB)
 k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float* __restrict__ targets, int T, const float* __restrict__ seeds,
@@ -93,7 +94,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     float rho_k = 1.f;   // delta_rho^k, by repeated multiplication (R5)
     int k;
     for (k = 0;; ++k, rho_k *= c.delta_rho) {
-        fk<NMAX, true, EXACT, true>(rb, th, P, Z, pe, qe);
+        fk<NMAX, true, EXACT, true, REV>(rb, th, P, Z, pe, qe);
         if constexpr (FRAMES_SMEM) {
             float2* s_fz = (float2*)(s_frames + NMAX * blockDim.x);
 #pragma unroll
@@ -152,7 +153,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
                 const DevJoint& J = rb.j[j];
                 const float3 z = Z[j];
                 float dp, sp, dor, so;
-                if (J.type == HJCD_REVOLUTE) {
+                if (REV || J.type == HJCD_REVOLUTE) {
                     // Eqs. 8-9 (R3): signed angle between the projections of
                     // u = P_ee - P_j and v = P_t - P_j on the plane normal to z_j;
                     // z.(u_p x v_p) = (z x u).v_p
@@ -215,8 +216,8 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         // frames of the two moved joints (uniform-index selects, no local memory);
         // an orientation winner is always revolute (prismatic candidates are 0)
         float3 Pa = f3(0.f, 0.f, 0.f), Za = Pa, Pb = Pa, Zb = Pa;
-        const int ta = (ja >= 0 && ((rb.pmask >> ja) & 1u)) ? HJCD_PRISMATIC : HJCD_REVOLUTE;
-        const int tb = ((rb.pmask >> jb) & 1u) ? HJCD_PRISMATIC : HJCD_REVOLUTE;
+        const int ta = (!REV && ja >= 0 && ((rb.pmask >> ja) & 1u)) ? HJCD_PRISMATIC : HJCD_REVOLUTE;
+        const int tb = (!REV && ((rb.pmask >> jb) & 1u)) ? HJCD_PRISMATIC : HJCD_REVOLUTE;
         if constexpr (FRAMES_SMEM) {
             const float2* s_fz = (const float2*)(s_frames + NMAX * blockDim.x);
             const float4 fb = s_frames[jb * blockDim.x + threadIdx.x];
@@ -306,8 +307,8 @@ static inline void texit_shape(int M, int& nt, int& CL) {
     CL = (M + nt - 1) / nt;
 }
 
-template <int NMAX, bool EXACT>
-cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+template <int NMAX, bool EXACT, bool REV>
+static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                   const float* seeds, float* theta, float* cost, float* ep, float* eo,
                                   int32_t* iters, cudaStream_t s) {
     if (!c.ccd_early_exit) {
@@ -315,7 +316,7 @@ cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* tar
         const int block = 128;
         const long long grid = (total + block - 1) / block;
         if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-        k_poccd<NMAX, EXACT, false><<<(unsigned)grid, block, poccd_smem<NMAX>(block), s>>>(
+        k_poccd<NMAX, EXACT, false, REV><<<(unsigned)grid, block, poccd_smem<NMAX>(block), s>>>(
             rb, c, targets, T, seeds, theta, cost, ep, eo, iters, 1);
         return cudaGetLastError();
     }
@@ -325,7 +326,7 @@ cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* tar
     if (CL > 8) {
         static bool np = false;
         if (!np) {
-            cudaError_t e = cudaFuncSetAttribute(k_poccd<NMAX, EXACT, true>,
+            cudaError_t e = cudaFuncSetAttribute(k_poccd<NMAX, EXACT, true, REV>,
                                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             if (e != cudaSuccess) return e;
             np = true;
@@ -345,8 +346,18 @@ cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* tar
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_poccd<NMAX, EXACT, true>, rb, c, targets, T, seeds, theta, cost, ep, eo,
+    return cudaLaunchKernelEx(&cfg, k_poccd<NMAX, EXACT, true, REV>, rb, c, targets, T, seeds, theta, cost, ep, eo,
                               iters, CL);
+}
+
+// all-revolute chains (the usual case) run the kernels without per-joint type branches
+template <int NMAX, bool EXACT>
+cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
+                           const float* seeds, float* theta, float* cost, float* ep, float* eo,
+                           int32_t* iters, cudaStream_t s) {
+    if (rb.pmask == 0u)
+        return launch_poccd_r<NMAX, EXACT, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+    return launch_poccd_r<NMAX, EXACT, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
 }
 
 }  // namespace hjcd
