@@ -56,7 +56,8 @@ size_t coop_smem_bytes(int nt) {
     return (size_t)nt * (8 + sizeof(T) * (4 * NMAX + 6 + 2) + 4 + 2 * 64);
 }
 
-template <class T, int NMAX, bool EXACT>
+// REV: every DoF joint is revolute (no per-joint type branches)
+template <class T, int NMAX, bool EXACT, bool REV>
 __global__ void __launch_bounds__(256)
 k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ DevCfg c,
             const float* __restrict__ targets, const float* __restrict__ seeds,
@@ -96,7 +97,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
         QuatT<T> qe;
         bool conv = false;
         if (live) {
-            fk<NMAX, true, EXACT>(rb, th, Jp, Jo, pe, qe);
+            fk<NMAX, true, EXACT, false, REV>(rb, th, Jp, Jo, pe, qe);
             r = residual(tg, pe, qe);
             conv = r.ep < T(c.eps_p_fine) && r.eo < T(c.eps_o_fine);   // Alg. 4 l.18 (R26)
         }
@@ -119,7 +120,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
             for (int j = 0; j < NMAX; ++j) {
                 if (EXACT || j < n) {
                     const vec3<T> z = Jo[j];
-                    if (rb.j[j].type == HJCD_REVOLUTE) {
+                    if (REV || rb.j[j].type == HJCD_REVOLUTE) {
                         Jp[j] = cross3(z, pe - Jp[j]);
                     } else {
                         Jp[j] = z;
@@ -228,7 +229,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                                             rb.j[j].hi)
                                    : T(0);
                 }
-                const ResidT<T> rt = eval_at<NMAX, EXACT>(rb, tg, x);
+                const ResidT<T> rt = eval_at<NMAX, EXACT, REV>(rb, tg, x);
                 bool ok;
                 if (kind == 1) {   // dogleg: unweighted |rho| (R23)
                     T nt2 = T(0);
@@ -298,22 +299,33 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
     if (iters_out) iters_out[row] = (c.target_early_exit || live) ? k : kseed;
 }
 
-template <class T, int NMAX, bool EXACT>
-cudaError_t launch_coop_t(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
-                          const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
-                          cudaStream_t s) {
+template <class T, int NMAX, bool EXACT, bool REV>
+static cudaError_t launch_coop_r(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
+                                 const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
+                                 cudaStream_t s) {
     const int used = c.copies * c.K;
     const int block = (used + 31) / 32 * 32;
     const size_t smem = coop_smem_bytes<T, NMAX>(block);
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pjik_coop<T, NMAX, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_pjik_coop<T, NMAX, EXACT, REV>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)coop_smem_bytes<T, NMAX>(256));
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_pjik_coop<T, NMAX, EXACT><<<T_, block, smem, s>>>(rb, c, targets, seeds, theta, ep, eo, counts, iters);
+    k_pjik_coop<T, NMAX, EXACT, REV><<<T_, block, smem, s>>>(rb, c, targets, seeds, theta, ep, eo, counts, iters);
     return cudaGetLastError();
+}
+
+// all-revolute chains run the kernel without per-joint type branches
+template <class T, int NMAX, bool EXACT>
+cudaError_t launch_coop_t(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
+                          const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
+                          cudaStream_t s) {
+    if (rb.pmask == 0u)
+        return launch_coop_r<T, NMAX, EXACT, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+    return launch_coop_r<T, NMAX, EXACT, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
 }
 
 }  // namespace hjcd

@@ -90,12 +90,12 @@ __device__ __forceinline__ T cost_w(const T (&W)[6], const T (&rho)[6]) {
     return T(0.5) * s;
 }
 
-template <int NMAX, bool EXACT = false, class T>
+template <int NMAX, bool EXACT = false, bool REV = false, class T>
 __device__ __forceinline__ ResidT<T> eval_at(const DevRobotT<T>& rb, const TargetT<T>& tg, const T (&th)[NMAX]) {
     vec3<T> P[NMAX], Z[NMAX];   // unused (FRAMES = false), eliminated
     vec3<T> pe;
     QuatT<T> qe;
-    fk<NMAX, false, EXACT>(rb, th, P, Z, pe, qe);
+    fk<NMAX, false, EXACT, false, REV>(rb, th, P, Z, pe, qe);
     return residual(tg, pe, qe);
 }
 
