@@ -1,6 +1,7 @@
 // dispatch.cu — picks the kernel instantiation for the robot's DoF: exact-N
-// kernels (no per-joint guards) for the benchmarked chains n = 7, 8, 14, and
-// NMAX-bounded kernels (uniform `j < n` guards) for every other n <= 32.
+// kernels (no per-joint guards) for the benchmarked chains n = 7, 8, 14 and
+// the paper's Table II DoFs 12, 18, 24, and NMAX-bounded kernels (uniform
+// `j < n` guards) for every other n <= 32.
 #include "hjcd_internal.h"
 
 namespace hjcd {
@@ -11,7 +12,10 @@ cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targe
     switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
         case 7: return launch_poccd_t<7, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
         case 8: return launch_poccd_t<8, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+        case 12: return launch_poccd_t<12, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
         case 14: return launch_poccd_t<14, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+        case 18: return launch_poccd_t<18, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+        case 24: return launch_poccd_t<24, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
         default: break;
     }
     if (rb.n <= 8) return launch_poccd_t<8, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
@@ -29,6 +33,14 @@ cudaError_t launch_pjik_coop(const DevRobotT<T>& rb, const DevCfg& c, const floa
         case 8: return launch_coop_t<T, 8, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
         case 14: return launch_coop_t<T, 14, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
         default: break;
+    }
+    if constexpr (sizeof(T) == 4) {   // Table II DoFs (fp32 polish only)
+        switch (rb.n) {
+            case 12: return launch_coop_t<T, 12, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+            case 18: return launch_coop_t<T, 18, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+            case 24: return launch_coop_t<T, 24, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+            default: break;
+        }
     }
     if (rb.n <= 8) return launch_coop_t<T, 8, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
     if (rb.n <= 16) return launch_coop_t<T, 16, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);

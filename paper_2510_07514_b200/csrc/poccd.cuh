@@ -30,11 +30,13 @@ namespace hjcd {
 //   (DSMEM stores, then barrier.cluster arrive.release / wait.acquire); all
 //   seeds of the target stop at the first iteration in which any seed passed.
 // REV: every DoF joint is revolute (no per-joint type branches).
-#ifndef HJCD_POCCD_MINB
-#define HJCD_POCCD_MINB 4
-#endif
+// Occupancy target: 4 CTAs of 128 (<= 128 registers) up to 14 joints; the
+// 16- and 32-joint bounds would spill 1-1.6 KB at 128, so they get 170 / 255.
+template <int NMAX>
+constexpr int poccd_min_blocks() { return NMAX <= 14 ? 4 : (NMAX <= 18 ? 3 : 2); }
+
 template <int NMAX, bool EXACT, bool TEXIT, bool REV>
-__global__ void __launch_bounds__(128, HJCD_POCCD_MINB)
+__global__ void __launch_bounds__(128, poccd_min_blocks<NMAX>())
 k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float* __restrict__ targets, int T, const float* __restrict__ seeds,
         float* __restrict__ theta_out, float* __restrict__ cost_out, float* __restrict__ ep_out,
@@ -46,7 +48,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     __shared__ int s_flag[3];
     // the frames (P_j, z_j) of this iteration, per thread, so the two moved
     // joints' frames are two indexed loads instead of 2 x NMAX predicated selects
-    constexpr bool FRAMES_SMEM = NMAX <= 16;
+    constexpr bool FRAMES_SMEM = NMAX <= 18;
     extern __shared__ float4 s_frames[];   // [NMAX][blockDim] (P.xyz, z.x), then float2 [NMAX][blockDim] (z.yz)
     if (TEXIT) {
         t = (int)(blockIdx.x / (unsigned)CL);
@@ -295,8 +297,8 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
 }
 
 template <int NMAX>
-inline size_t poccd_smem(int nt) {   // the per-thread frames (24 B per joint) for NMAX <= 16
-    return NMAX <= 16 ? (size_t)NMAX * nt * (sizeof(float4) + sizeof(float2)) : 0;
+inline size_t poccd_smem(int nt) {   // the per-thread frames (24 B per joint) for NMAX <= 18
+    return NMAX <= 18 ? (size_t)NMAX * nt * (sizeof(float4) + sizeof(float2)) : 0;
 }
 
 // seeds per CTA (nt) and CTAs per cluster (CL) of the lockstep launch:
@@ -311,6 +313,16 @@ template <int NMAX, bool EXACT, bool REV>
 static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                   const float* seeds, float* theta, float* cost, float* ep, float* eo,
                                   int32_t* iters, cudaStream_t s) {
+    static bool smem_attr = false;   // NMAX = 16: the frames copy is 48 KB, above the default limit
+    if (!smem_attr && poccd_smem<NMAX>(128) > 0) {
+        cudaError_t e;
+        if ((e = cudaFuncSetAttribute(k_poccd<NMAX, EXACT, false, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)poccd_smem<NMAX>(128))) != cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_poccd<NMAX, EXACT, true, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)poccd_smem<NMAX>(128))) != cudaSuccess)
+            return e;
+        smem_attr = true;
+    }
     if (!c.ccd_early_exit) {
         const long long total = (long long)T * c.M;
         const int block = 128;

@@ -12,7 +12,8 @@ from paper_2510_07514_b200 import hjcd, inputs
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-rname, T = {"c2": ("panda", 1000), "c3": ("fetch_like8", 10000), "c4": ("panda_x14", 10000)}[cfgname]
+CFG = {"c2": ("panda", 1000), "c3": ("fetch_like8", 10000), "c4": ("panda_x14", 10000)}
+rname, T = CFG[cfgname] if cfgname in CFG else (cfgname, 1000)   # e.g. panda_x12: 1000 targets
 chain = inputs.robot(rname)
 robot = hjcd.Robot(chain)
 dev = torch.device("cuda", 0)

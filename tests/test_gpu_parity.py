@@ -538,7 +538,7 @@ def test_maximum_sizes(hjcd_lib, cuda):
         hjcd_lib.solve(rb7, T(tg7, cuda), hjcd_lib.config_from_params(params(K=50, B=300)))
 
 
-@pytest.mark.parametrize("name", ["fetch", "panda_x14", "panda_x24"])
+@pytest.mark.parametrize("name", ["fetch", "panda_x12", "panda_x14", "panda_x16", "panda_x18", "panda_x24"])
 def test_solve_other_chains(hjcd_lib, cuda, name):
     ch = inputs.robot(name)
     rb = hjcd_lib.Robot(ch)
