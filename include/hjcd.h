@@ -198,7 +198,9 @@ hjcd_status hjcd_fk(const hjcd_robot* r, const float* q, int32_t N, float* pose7
 /* PO-CCD (Alg. 3) for T targets x c->M seeds.
  *   seeds  [T][dof][M] initial theta, or NULL = Philox uniform in limits (Alg. 3 l.2-3)
  *   theta  [T][dof][M] out; cost [T][M] out: w_p^2 |r_p|^2 + w_o^2 |omega|^2 (R14)
- *   pos_err, ori_err [T][M] out or NULL; iters [T][M] out or NULL (updates applied). */
+ *   pos_err, ori_err [T][M] out or NULL; iters [T][M] out or NULL (updates applied;
+ *   with c->ccd_early_exit every seed of a target reports the target's k*, R12b,
+ *   and M <= 2048, else E_UNSUPPORTED). */
 hjcd_status hjcd_poccd(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
                        const float* seeds, float* theta, float* cost, float* pos_err,
                        float* ori_err, int32_t* iters, hjcd_stream_t stream);
