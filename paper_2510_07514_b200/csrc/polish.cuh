@@ -107,17 +107,27 @@ __device__ __forceinline__ bool lm_direction(const DevRobotT<T>& rb, const DevCf
                                              const vec3<T> (&Jo)[NMAX], const T (&invD)[NMAX],
                                              const T (&W)[6], const T (&rho)[6], T (&dth)[NMAX]) {
     const int n = rb.n;
+    // G = sum_j (J_j / D_j) J_j^T: scale each column once, then one FMA per term
     T A[21];
+#pragma unroll
+    for (int q = 0; q < 21; ++q) A[q] = T(0);
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) {
+        if (EXACT || j < n) {
+            const T col[6] = {Jp[j].x, Jp[j].y, Jp[j].z, Jo[j].x, Jo[j].y, Jo[j].z};
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                const T ui = col[i] * invD[j];
+#pragma unroll
+                for (int kk = 0; kk <= i; ++kk) A[i * (i + 1) / 2 + kk] += ui * col[kk];
+            }
+        }
+    }
 #pragma unroll
     for (int i = 0; i < 6; ++i)
 #pragma unroll
-        for (int kk = 0; kk <= i; ++kk) {
-            T s = T(0);
-#pragma unroll
-            for (int j = 0; j < NMAX; ++j)
-                if (EXACT || j < n) s += jrow(Jp[j], Jo[j], i) * jrow(Jp[j], Jo[j], kk) * invD[j];
-            A[i * (i + 1) / 2 + kk] = W[i] * W[kk] * s + (i == kk ? T(c.lambda) : T(0));
-        }
+        for (int kk = 0; kk <= i; ++kk)
+            A[i * (i + 1) / 2 + kk] = W[i] * W[kk] * A[i * (i + 1) / 2 + kk] + (i == kk ? T(c.lambda) : T(0));
     T y[6];
 #pragma unroll
     for (int i = 0; i < 6; ++i) y[i] = W[i] * rho[i];
