@@ -205,6 +205,18 @@ hjcd_status hjcd_poccd(const hjcd_robot* r, const hjcd_config* c, const float* t
                        const float* seeds, float* theta, float* cost, float* pos_err,
                        float* ori_err, int32_t* iters, hjcd_stream_t stream);
 
+/* hjcd_poccd that also records every seed's decisions (parity tests: the
+ * oracle replays them in fp64): trace [T][M][c->ccd_iters]
+ * uint32, one word per iteration k that updated the seed (entries past its
+ * iteration count are left unwritten):
+ *   bits 0-4 jp, 5-9 jo (Alg. 3 l.9 argmins), bit 10 same joint and the
+ *   orientation step taken (l.10), bit 11 accepted (l.11), bits 12-13 / 14-15
+ *   the sign of the position / orientation step at jp / jo (0 zero,
+ *   1 positive, 2 negative). */
+hjcd_status hjcd_poccd_trace(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                             const float* seeds, float* theta, float* cost, float* pos_err,
+                             float* ori_err, int32_t* iters, uint32_t* trace, hjcd_stream_t stream);
+
 /* Classic position-only CCD (Alg. 1), the baseline PO-CCD extends
  * (ablation): T targets x c->M seeds, joints swept tip to root,
  * signed projected-angle steps (Eqs. 8-9; R3, R4) clamped to the limits (R7);

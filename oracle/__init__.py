@@ -75,8 +75,9 @@ def lib():
         _lib.oracle_ccd_orientation_step.argtypes = [P, P, P, P, i32]
         _lib.oracle_uniform_seeds.argtypes = [P, u64, i64, i32, P]
         _lib.oracle_fk.argtypes = [P, P, i32, P, P, P, P]
-        _lib.oracle_po_ccd.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P]
+        _lib.oracle_po_ccd.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P, P]
         _lib.oracle_ccd.argtypes = [P, P, P, i32, i64, P, P, P, P]
+        _lib.oracle_po_ccd_replay.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P, P]
         _lib.oracle_select_replicate.argtypes = [P, P, P, P, i32, i64, P, P]
         _lib.oracle_pj_ik.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P]
         _lib.oracle_solve.argtypes = [P, P, P, i32, i64, P, P, P, P]
@@ -244,9 +245,10 @@ def line_search(chain, params, target7, theta, dth) -> int:
 
 
 # ---------------------------------------------------------------- stages
-def po_ccd(chain, params, targets, tid_offset: int = 0, seeds: Optional[np.ndarray] = None):
+def po_ccd(chain, params, targets, tid_offset: int = 0, seeds: Optional[np.ndarray] = None,
+           trace: bool = False):
     """Alg. 3 for T x M seeds.  Returns dict of theta [T,n,M], cost, ep, eo,
-    iters, margin [T,M]."""
+    iters, margin [T,M] (+ trace [T,M,ccd_iters]: its own decision words)."""
     r, c = make_robot(chain), make_config(params)
     tg = np.ascontiguousarray(targets, dtype=np.float32).reshape(-1, 7)
     T, n, M = tg.shape[0], chain.dof, params["M"]
@@ -254,9 +256,30 @@ def po_ccd(chain, params, targets, tid_offset: int = 0, seeds: Optional[np.ndarr
     out = dict(theta=np.empty((T, n, M)), cost=np.empty((T, M)), ep=np.empty((T, M)),
                eo=np.empty((T, M)), iters=np.empty((T, M), dtype=np.int32),
                margin=np.empty((T, M)))
+    if trace:
+        out["trace"] = np.zeros((T, M, max(params["ccd_iters"], 1)), dtype=np.uint32)
     lib().oracle_po_ccd(_ref(r), _ref(c), _p(tg), T, tid_offset, _p(sd), _p(out["theta"]),
                         _p(out["cost"]), _p(out["ep"]), _p(out["eo"]), _p(out["iters"]),
-                        _p(out["margin"]))
+                        _p(out["margin"]), _p(out.get("trace")))
+    return out
+
+
+def po_ccd_replay(chain, params, targets, trace, iters, tid_offset: int = 0):
+    """Alg. 3 in fp64 following recorded decisions (hjcd_poccd_trace words,
+    trace [T,M,ccd_iters] uint32, iters [T,M]) -> dict theta [T,n,M], ep, eo,
+    gap [T,M] (how much worse any recorded decision is than the fp64 one) and
+    stop_gap [T] (how far outside the coarse box the GPU stopped), gap_at [T,M]
+    (8 k + kind of the largest gap: 1 jp, 2 jo, 3 same joint, 4 gamma, 5 stop; -1 none)."""
+    r, c = make_robot(chain), make_config(params)
+    tg = np.ascontiguousarray(targets, dtype=np.float32).reshape(-1, 7)
+    T, n, M = tg.shape[0], chain.dof, params["M"]
+    tr = np.ascontiguousarray(trace, dtype=np.uint32).reshape(T, M, params["ccd_iters"])
+    it = np.ascontiguousarray(iters, dtype=np.int32).reshape(T, M)
+    out = dict(theta=np.empty((T, n, M)), ep=np.empty((T, M)), eo=np.empty((T, M)),
+               gap=np.empty((T, M)), stop_gap=np.empty(T), gap_at=np.empty((T, M), dtype=np.int32))
+    lib().oracle_po_ccd_replay(_ref(r), _ref(c), _p(tg), T, tid_offset, _p(tr), _p(it), _p(out["theta"]),
+                               _p(out["ep"]), _p(out["eo"]), _p(out["gap"]), _p(out["stop_gap"]),
+                               _p(out["gap_at"]))
     return out
 
 

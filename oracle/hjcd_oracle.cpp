@@ -448,7 +448,8 @@ bool po_ccd_check(const Robot& rb, const OracleConfig& c, const Target& tgt,
  * at iteration k (frames F and residual e at th), or a perturbation. */
 void po_ccd_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
                  uint32_t sid, int k, const Frames& F, const Err& e, std::vector<double>& th,
-                 SeedOut& so) {
+                 SeedOut& so, const uint32_t* forced = nullptr, double* gap = nullptr,
+                 uint32_t* record = nullptr, int* gap_kind = nullptr) {
     const OracleRobot* r = rb.r;
     int n = rb.dof;
     Frames Fc;
@@ -459,6 +460,11 @@ void po_ccd_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint
     /* the w >= 0 canonicalisation of q_err flips a (R1/R2) when w crosses 0 */
     if (phi > 0) so.margin = std::min(so.margin, std::fabs(std::cos(phi / 2.0)));
     std::vector<double> sp(n), sop(n), dp(n), dor(n);
+    /* replay only: the other sign of each candidate step, its score, and how
+     * near its sign is to a tie: the pi branch cut of Eq. 9 (pi - |step|),
+     * sgn(a . r_j) of Eq. 11 near 0 (|a . r_j|), or a vanishing step (|step|) */
+    std::vector<double> dpa, spa, doa, sopa, tp(n, INF), to(n, INF);
+    if (forced) { dpa.assign(n, 0.0); spa.assign(n, 0.0); doa.assign(n, 0.0); sopa.assign(n, 0.0); }
     for (int j = 0; j < n; ++j) {
         int ent = rb.dof_entry[j];
         double lo = r->lo[ent], hi = r->hi[ent];
@@ -476,6 +482,16 @@ void po_ccd_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint
         thc = th; thc[j] = th[j] + dp[j];
         fk(rb, thc.data(), Fc);                     /* literal P:222: full FK */
         sp[j] = norm(sub(tgt.p, Fc.pee));
+        if (forced) {
+            dpa[j] = dp[j]; spa[j] = sp[j];
+            if (r->type[ent] == 0 && stepp != 0.0) {
+                tp[j] = std::min(PI - std::fabs(stepp), std::fabs(stepp));
+                dpa[j] = clampd(th[j] - stepp, lo, hi) - th[j];
+                thc = th; thc[j] = th[j] + dpa[j];
+                fk(rb, thc.data(), Fc);
+                spa[j] = norm(sub(tgt.p, Fc.pee));
+            }
+        }
         /* orientation candidate (Eqs. 10-11); prismatic: 0 */
         double stepo = 0.0;
         if (r->type[ent] == 0) {
@@ -486,6 +502,16 @@ void po_ccd_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint
         thc = th; thc[j] = th[j] + dor[j];
         fk(rb, thc.data(), Fc);
         sop[j] = norm(quat_error(tgt.q, Fc.qee));
+        if (forced) {
+            doa[j] = dor[j]; sopa[j] = sop[j];
+            if (r->type[ent] == 0 && phi > 0) {
+                to[j] = std::min(std::fabs(dot(ahat, F.z[j])), std::fabs(stepo));
+                doa[j] = clampd(th[j] - stepo, lo, hi) - th[j];
+                thc = th; thc[j] = th[j] + doa[j];
+                fk(rb, thc.data(), Fc);
+                sopa[j] = norm(quat_error(tgt.q, Fc.qee));
+            }
+        }
     }
     /* Alg. 3 l.9: argmin over joints, ties -> lower index (R6) */
     int jp = 0, jo = 0;
@@ -500,12 +526,53 @@ void po_ccd_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint
         if (j != jo && (dor[j] != 0.0 || dor[jo] != 0.0))
             so.margin = std::min(so.margin, std::fabs(sop[j] - sop[jo]));
     }
+    /* replay (oracle_po_ccd_replay): take the recorded argmins instead; the gap
+     * is how much worse they score than this fp64 argmin */
+    if (forced) {
+        auto upd = [&](double g, int kind) { if (g > *gap) { *gap = g; *gap_kind = kind; } };
+        auto code = [](double x) { return x > 0 ? 1u : (x < 0 ? 2u : 0u); };
+        int fp = (int)(*forced & 31u), fo = (int)((*forced >> 5) & 31u);
+        if (fp >= n || fo >= n) { *gap = INF; return; }
+        /* the recorded step signs: a near-tie sign takes the other variant
+         * (gap = the tie's distance); a sign no variant has costs |step| */
+        unsigned cp = (*forced >> 12) & 3u, co = (*forced >> 14) & 3u;
+        if (code(dp[fp]) != cp) {
+            if (code(dpa[fp]) == cp) { upd(tp[fp], 6); dp[fp] = dpa[fp]; sp[fp] = spa[fp]; }
+            else upd(std::fabs(dp[fp]), 6);
+        }
+        if (code(dor[fo]) != co) {
+            if (code(doa[fo]) == co) { upd(to[fo], 7); dor[fo] = doa[fo]; sop[fo] = sopa[fo]; }
+            else upd(std::fabs(dor[fo]), 7);
+        }
+        /* the best score any valid reading allows: a near-tie joint counts
+         * with its worse variant */
+        const double TIE = 1e-4;
+        double bp = INF, bo = INF;
+        for (int j = 0; j < n; ++j) {
+            bp = std::min(bp, j != fp && tp[j] < TIE ? std::max(sp[j], spa[j]) : sp[j]);
+            bo = std::min(bo, j != fo && to[j] < TIE ? std::max(sop[j], sopa[j]) : sop[j]);
+        }
+        upd(sp[fp] - bp, 1);
+        upd(sop[fo] - bo, 2);
+        jp = fp;
+        jo = fo;
+    }
     /* Alg. 3 l.10 + P:201: same joint -> larger |dtheta|, tie -> position (R8) */
     thh = th;
+    bool ori_taken = false;
     if (jp == jo) {
         if (dp[jp] != dor[jo]) /* equal steps = same outcome, no decision */
             so.margin = std::min(so.margin, std::fabs(std::fabs(dp[jp]) - std::fabs(dor[jo])));
-        if (std::fabs(dp[jp]) >= std::fabs(dor[jo])) thh[jp] = th[jp] + dp[jp];
+        bool take_p = std::fabs(dp[jp]) >= std::fabs(dor[jo]);
+        if (forced && dp[jp] != dor[jo] && take_p == (((*forced >> 10) & 1u) != 0)) {
+            if (std::fabs(std::fabs(dp[jp]) - std::fabs(dor[jo])) > *gap) {
+                *gap = std::fabs(std::fabs(dp[jp]) - std::fabs(dor[jo]));
+                *gap_kind = 3;
+            }
+            take_p = !take_p;
+        }
+        ori_taken = !take_p;
+        if (take_p) thh[jp] = th[jp] + dp[jp];
         else thh[jo] = th[jo] + dor[jo];
     } else {
         thh[jp] = th[jp] + dp[jp];
@@ -521,9 +588,18 @@ void po_ccd_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint
     /* Alg. 3 l.11 read as an improvement test on either space (R10) */
     double ip = e.ep - eh.ep, io = e.eo - eh.eo;
     bool ap = ip > c.gamma, ao = io > c.gamma;
-    so.margin = std::min(so.margin, margin_or(ap, std::fabs(ip - c.gamma), ao,
-                                              std::fabs(io - c.gamma)));
-    if (ap || ao) {
+    double macc = margin_or(ap, std::fabs(ip - c.gamma), ao, std::fabs(io - c.gamma));
+    so.margin = std::min(so.margin, macc);
+    bool accept = ap || ao;
+    if (forced && accept != (((*forced >> 11) & 1u) != 0)) {
+        if (macc > *gap) { *gap = macc; *gap_kind = 4; }
+        accept = !accept;
+    }
+    if (record)   /* this oracle's own decisions, in hjcd_poccd_trace's word format */
+        *record = (uint32_t)jp | ((uint32_t)jo << 5) | (ori_taken ? 1u << 10 : 0u) |
+                  (accept ? 1u << 11 : 0u) | ((dp[jp] > 0 ? 1u : dp[jp] < 0 ? 2u : 0u) << 12) |
+                  ((dor[jo] > 0 ? 1u : dor[jo] < 0 ? 2u : 0u) << 14);
+    if (accept) {
         th = thh;
     } else {
         /* Alg. 3 l.13: theta + N(0, sigma_ccd^2 I), clamp (R11) */
@@ -545,7 +621,7 @@ SeedOut seed_init() {
 
 /* Alg. 3 for ONE seed with a per-seed break (ccd_early_exit = 0) */
 SeedOut po_ccd_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
-                    uint32_t sid, std::vector<double>& th) {
+                    uint32_t sid, std::vector<double>& th, uint32_t* record = nullptr) {
     SeedOut so = seed_init();
     Frames F;
     Err e;
@@ -553,7 +629,7 @@ SeedOut po_ccd_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, u
     for (k = 0;; ++k) {
         if (po_ccd_check(rb, c, tgt, th, F, e, so)) break;
         if (k == c.ccd_iters) break;
-        po_ccd_step(rb, c, tgt, tid, sid, k, F, e, th, so);
+        po_ccd_step(rb, c, tgt, tid, sid, k, F, e, th, so, nullptr, nullptr, record ? record + k : nullptr);
     }
     so.iters = k;
     return so;
@@ -567,7 +643,8 @@ SeedOut po_ccd_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, u
  * passes the coarse test, every seed keeping its state after that many
  * iterations.  th_m: [M][n] in/out. */
 void po_ccd_target(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid, int M,
-                   std::vector<std::vector<double>>& th_m, std::vector<SeedOut>& so) {
+                   std::vector<std::vector<double>>& th_m, std::vector<SeedOut>& so,
+                   uint32_t* record = nullptr) {
     so.assign(M, seed_init());
     std::vector<Frames> F(M);
     std::vector<Err> e(M);
@@ -579,7 +656,9 @@ void po_ccd_target(const Robot& rb, const OracleConfig& c, const Target& tgt, ui
         }
         for (int m = 0; m < M; ++m) so[m].iters = k;
         if (any || k == c.ccd_iters) break;
-        for (int m = 0; m < M; ++m) po_ccd_step(rb, c, tgt, tid, (uint32_t)m, k, F[m], e[m], th_m[m], so[m]);
+        for (int m = 0; m < M; ++m)
+            po_ccd_step(rb, c, tgt, tid, (uint32_t)m, k, F[m], e[m], th_m[m], so[m], nullptr, nullptr,
+                        record ? record + (size_t)m * c.ccd_iters + k : nullptr);
     }
 }
 
@@ -1085,7 +1164,7 @@ double oracle_normal(uint64_t seed, int64_t tid, uint32_t sid, uint32_t purpose,
  * margin f64 [T][M] (smallest absolute decision margin along the trajectory). */
 void oracle_po_ccd(const OracleRobot* r, const OracleConfig* c, const float* targets, int32_t T,
                    int64_t tid_offset, const double* seeds, double* theta, double* cost,
-                   double* ep, double* eo, int32_t* iters, double* margin) {
+                   double* ep, double* eo, int32_t* iters, double* margin, uint32_t* trace) {
     Robot rb = make_robot(r);
     int n = rb.dof, M = c->M;
     auto seed_of = [&](int t, int m, uint64_t tid, std::vector<double>& th) {
@@ -1109,7 +1188,7 @@ void oracle_po_ccd(const OracleRobot* r, const OracleConfig* c, const float* tar
             std::vector<std::vector<double>> th(M, std::vector<double>(n));
             for (int m = 0; m < M; ++m) seed_of(t, m, tid, th[m]);
             std::vector<SeedOut> so;
-            po_ccd_target(rb, *c, tgt, tid, M, th, so);
+            po_ccd_target(rb, *c, tgt, tid, M, th, so, trace ? trace + (size_t)t * M * c->ccd_iters : nullptr);
             for (int m = 0; m < M; ++m) emit(t, m, th[m], so[m]);
         }
         return;
@@ -1121,9 +1200,77 @@ void oracle_po_ccd(const OracleRobot* r, const OracleConfig* c, const float* tar
             uint64_t tid = (uint64_t)(tid_offset + t);
             std::vector<double> th(n);
             seed_of(t, m, tid, th);
-            SeedOut so = po_ccd_seed(rb, *c, tgt, tid, (uint32_t)m, th);
+            SeedOut so = po_ccd_seed(rb, *c, tgt, tid, (uint32_t)m, th,
+                                     trace ? trace + ((size_t)t * M + m) * c->ccd_iters : nullptr);
             emit(t, m, th, so);
         }
+    }
+}
+
+/* Decision replay of Alg. 3 (parity tests, DESIGN.md §4 "decision replay"):
+ * every seed runs the GPU's iteration count iters [T][M] and, at each
+ * iteration k, takes the GPU's recorded decisions trace [T][M][ccd_iters]
+ * (hjcd_poccd_trace word: jp | jo << 5 | orientation-taken << 10 |
+ * accepted << 11 | position / orientation step sign << 12 / 14) in place of
+ * its own, with every candidate, score, step and
+ * the perturbation computed here in fp64 exactly as in po_ccd_step.
+ *   gap [T][M]: the largest amount by which a recorded decision is worse than
+ *     this oracle's own (a score difference in m or rad, |dp| - |do| in rad,
+ *     the distance of the gamma test from its threshold; 0 = all agree), and
+ *     the depth inside the coarse box at an iteration the GPU continued;
+ *   gap_at [T][M] (or NULL): 8 k + kind of that largest gap (kind 1 jp, 2 jo,
+ *     3 same-joint choice, 4 gamma test, 5 continued inside the box, 6 / 7
+ *     the sign of the position / orientation step), -1 none;
+ *   stop_gap [T]: the distance outside the coarse box of the seed closest to
+ *     it where the GPU stopped before ccd_iters (per target with
+ *     ccd_early_exit, else the max over the seeds of their own); 0 if none.
+ * theta f64 [T][n][M], ep/eo f64 [T][M] after the replay. */
+void oracle_po_ccd_replay(const OracleRobot* r, const OracleConfig* c, const float* targets, int32_t T,
+                          int64_t tid_offset, const uint32_t* trace, const int32_t* iters,
+                          double* theta, double* ep, double* eo, double* gap, double* stop_gap,
+                          int32_t* gap_at) {
+    Robot rb = make_robot(r);
+    int n = rb.dof, M = c->M, I = c->ccd_iters;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int t = 0; t < T; ++t) {
+        Target tgt = read_target(targets + (size_t)t * 7);
+        uint64_t tid = (uint64_t)(tid_offset + t);
+        double sg = c->ccd_early_exit ? INF : 0.0;
+        bool stopped = false;
+        for (int m = 0; m < M; ++m) {
+            size_t o = (size_t)t * M + m;
+            std::vector<double> th(n);
+            uniform_seed(rb, c->rng_seed, tid, (uint32_t)m, th.data());
+            SeedOut so = seed_init();
+            Frames F;
+            Err e;
+            double g = 0.0;
+            int K = iters[o], kind = 0, at = -1;
+            for (int k = 0;; ++k) {
+                po_ccd_check(rb, *c, tgt, th, F, e, so);
+                double inside = std::min(c->eps_p_coarse - e.ep, c->eps_o_coarse - e.eo);
+                if (k == K) {
+                    if (K < I) {
+                        double outside = std::max(0.0, -inside);
+                        stopped = true;
+                        sg = c->ccd_early_exit ? std::min(sg, outside) : std::max(sg, outside);
+                    }
+                    break;
+                }
+                if (inside > g) { g = inside; at = 8 * k + 5; }
+                kind = 0;
+                double g0 = g;
+                po_ccd_step(rb, *c, tgt, tid, (uint32_t)m, k, F, e, th, so, trace + o * I + k, &g, nullptr, &kind);
+                if (g > g0) at = 8 * k + kind;
+                if (!std::isfinite(g)) break;
+            }
+            for (int j = 0; j < n; ++j) theta[((size_t)t * n + j) * M + m] = th[j];
+            ep[o] = so.ep;
+            eo[o] = so.eo;
+            gap[o] = g;
+            if (gap_at) gap_at[o] = at;
+        }
+        stop_gap[t] = stopped ? sg : 0.0;
     }
 }
 

@@ -8,19 +8,19 @@ namespace hjcd {
 
 cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                          const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                         int32_t* iters, cudaStream_t s) {
+                         int32_t* iters, cudaStream_t s, uint32_t* trace) {
     switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
-        case 7: return launch_poccd_t<7, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-        case 8: return launch_poccd_t<8, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-        case 12: return launch_poccd_t<12, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-        case 14: return launch_poccd_t<14, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-        case 18: return launch_poccd_t<18, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-        case 24: return launch_poccd_t<24, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+        case 7: return launch_poccd_t<7, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
+        case 8: return launch_poccd_t<8, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
+        case 12: return launch_poccd_t<12, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
+        case 14: return launch_poccd_t<14, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
+        case 18: return launch_poccd_t<18, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
+        case 24: return launch_poccd_t<24, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
         default: break;
     }
-    if (rb.n <= 8) return launch_poccd_t<8, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-    if (rb.n <= 16) return launch_poccd_t<16, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-    return launch_poccd_t<32, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+    if (rb.n <= 8) return launch_poccd_t<8, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
+    if (rb.n <= 16) return launch_poccd_t<16, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
+    return launch_poccd_t<32, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
 }
 
 template <class T>

@@ -540,6 +540,19 @@ hjcd_status hjcd_ccd(const hjcd_robot* r, const hjcd_config* c, const float* tar
     return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
 }
 
+hjcd_status hjcd_poccd_trace(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                             const float* seeds, float* theta, float* cost, float* pos_err, float* ori_err,
+                             int32_t* iters, uint32_t* trace, hjcd_stream_t stream) {
+    if (!r || !c || !targets || T < 1 || !theta || !cost || !trace) return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    if ((st = check_poccd(c)) != HJCD_OK) return st;
+    cudaError_t e = launch_poccd(r->dev, d, targets, T, seeds, theta, cost, pos_err, ori_err, iters,
+                                 (cudaStream_t)stream, trace);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+}
+
 hjcd_status hjcd_select_replicate(const hjcd_robot* r, const hjcd_config* c, const float* cost,
                                   const float* theta, int32_t T, float* polish_seeds, int32_t* kept_idx,
                                   hjcd_stream_t stream) {

@@ -57,7 +57,7 @@ enum : uint32_t { P_INIT = 1, P_PERTURB = 2, P_REPL = 3, P_PJPERT = 4 };
 template <int NMAX, bool EXACT>
 cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                            const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                           int32_t* iters, cudaStream_t s);
+                           int32_t* iters, uint32_t* trace, cudaStream_t s);
 template <int NMAX, bool EXACT>
 cudaError_t launch_ccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* seeds,
                          float* theta, float* ep, int32_t* iters, cudaStream_t s);
@@ -71,7 +71,7 @@ cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, f
                       cudaStream_t s);
 cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                          const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                         int32_t* iters, cudaStream_t s);
+                         int32_t* iters, cudaStream_t s, uint32_t* trace = nullptr);
 cudaError_t launch_ccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* seeds,
                        float* theta, float* ep, int32_t* iters, cudaStream_t s);
 cudaError_t launch_select_replicate(const DevRobot& rb, const DevCfg& c, const float* cost,

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(128, poccd_min_blocks<NMAX>())
 k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float* __restrict__ targets, int T, const float* __restrict__ seeds,
         float* __restrict__ theta_out, float* __restrict__ cost_out, float* __restrict__ ep_out,
-        float* __restrict__ eo_out, int32_t* __restrict__ iters_out, int CL) {
+        float* __restrict__ eo_out, int32_t* __restrict__ iters_out, int CL, uint32_t* __restrict__ trace) {
     const int M = c.M;
     const int n = rb.n;
     int t, m;
@@ -271,7 +271,13 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float ep_h = sqrtf(dot3(rh, rh));
         const float eo_h = 2.f * fast_atan2f(sqrtf(q2.x * q2.x + q2.y * q2.y + q2.z * q2.z), fabsf(q2.w));
         // ---- Alg. 3 l.11-13 (R10): accept on an improvement > gamma in either space
-        if ((ep - ep_h) > c.gamma || (eo - eo_h) > c.gamma) {
+        const bool accept = (ep - ep_h) > c.gamma || (eo - eo_h) > c.gamma;
+        if (trace && active)   // decision word: see hjcd_poccd_trace (include/hjcd.h)
+            trace[((long long)t * M + m) * c.ccd_iters + k] =
+                (uint32_t)jp | ((uint32_t)jo << 5) | ((jp == jo && db != dp_best) ? 1u << 10 : 0u) |
+                (accept ? 1u << 11 : 0u) | ((dp_best > 0.f ? 1u : dp_best < 0.f ? 2u : 0u) << 12) |
+                ((do_best > 0.f ? 1u : do_best < 0.f ? 2u : 0u) << 14);
+        if (accept) {
 #pragma unroll
             for (int j = 0; j < NMAX; ++j) {
                 if (EXACT || j < n) {
@@ -312,7 +318,7 @@ static inline void texit_shape(int M, int& nt, int& CL) {
 template <int NMAX, bool EXACT, bool REV>
 static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                   const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                                  int32_t* iters, cudaStream_t s) {
+                                  int32_t* iters, uint32_t* trace, cudaStream_t s) {
     static bool smem_attr = false;   // NMAX = 16: the frames copy is 48 KB, above the default limit
     if (!smem_attr && poccd_smem<NMAX>(128) > 0) {
         cudaError_t e;
@@ -329,7 +335,7 @@ static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const flo
         const long long grid = (total + block - 1) / block;
         if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
         k_poccd<NMAX, EXACT, false, REV><<<(unsigned)grid, block, poccd_smem<NMAX>(block), s>>>(
-            rb, c, targets, T, seeds, theta, cost, ep, eo, iters, 1);
+            rb, c, targets, T, seeds, theta, cost, ep, eo, iters, 1, trace);
         return cudaGetLastError();
     }
     int nt, CL;
@@ -359,17 +365,17 @@ static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const flo
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k_poccd<NMAX, EXACT, true, REV>, rb, c, targets, T, seeds, theta, cost, ep, eo,
-                              iters, CL);
+                              iters, CL, trace);
 }
 
 // all-revolute chains (the usual case) run the kernels without per-joint type branches
 template <int NMAX, bool EXACT>
 cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                            const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                           int32_t* iters, cudaStream_t s) {
+                           int32_t* iters, uint32_t* trace, cudaStream_t s) {
     if (rb.pmask == 0u)
-        return launch_poccd_r<NMAX, EXACT, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
-    return launch_poccd_r<NMAX, EXACT, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, s);
+        return launch_poccd_r<NMAX, EXACT, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
+    return launch_poccd_r<NMAX, EXACT, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
 }
 
 }  // namespace hjcd

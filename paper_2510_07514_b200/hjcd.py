@@ -26,7 +26,7 @@ EXPORTS = [
     "hjcd_robot_limits", "hjcd_config_default", "hjcd_workspace_size",
     "hjcd_workspace_size_host", "hjcd_solve", "hjcd_solve_timed", "hjcd_solve_host", "hjcd_ccd",
     "hjcd_solve_batch", "hjcd_select_topn", "hjcd_mmd", "hjcd_workspace_size_f64", "hjcd_solve_f64",
-    "hjcd_pjik_f64", "hjcd_fk", "hjcd_poccd",
+    "hjcd_pjik_f64", "hjcd_fk", "hjcd_poccd", "hjcd_poccd_trace",
     "hjcd_select_replicate", "hjcd_pjik", "hjcd_select_best", "hjcd_status_string",
     "hjcd_last_cuda_error", "hjcd_version",
 ]
@@ -83,6 +83,7 @@ def lib():
         L.hjcd_solve_host.argtypes = [P, P, P, i32, P, P, P, P, P, sz, P]
         L.hjcd_fk.argtypes = [P, P, i32, P, P, P]
         L.hjcd_poccd.argtypes = [P, P, P, i32, P, P, P, P, P, P, P]
+        L.hjcd_poccd_trace.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P]
         L.hjcd_ccd.argtypes = [P, P, P, i32, P, P, P, P, P]
         L.hjcd_solve_batch.argtypes = [P, P, P, i32, i32, P, P, P, P, P, sz, P]
         L.hjcd_select_topn.argtypes = [P, P, P, i32, P, P, P, i32, P, P, P, P, P]
@@ -416,6 +417,27 @@ def poccd(robot: Robot, cfg: hjcd_config, targets, seeds=None, stream=None):
     _check(lib().hjcd_poccd(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(seeds),
                             _ptr(out["theta"]), _ptr(out["cost"]), _ptr(out["ep"]),
                             _ptr(out["eo"]), _ptr(out["iters"]), _stream(stream)), "hjcd_poccd")
+    return out
+
+
+def poccd_trace(robot: Robot, cfg: hjcd_config, targets, seeds=None, stream=None):
+    """hjcd_poccd that also returns every seed's decision words:
+    trace [T, M, ccd_iters] uint32 (as int32), unwritten past iters = 0."""
+    torch = _torch()
+    T, n, M = targets.shape[0], robot.dof, cfg.M
+    _dev_f32(targets, (T, 7), "targets")
+    if seeds is not None:
+        _dev_f32(seeds, (T, n, M), "seeds")
+    d = targets.device
+    out = dict(theta=torch.empty((T, n, M), dtype=torch.float32, device=d),
+               cost=torch.empty((T, M), dtype=torch.float32, device=d),
+               ep=torch.empty((T, M), dtype=torch.float32, device=d),
+               eo=torch.empty((T, M), dtype=torch.float32, device=d),
+               iters=torch.empty((T, M), dtype=torch.int32, device=d),
+               trace=torch.zeros((T, M, max(cfg.ccd_iters, 1)), dtype=torch.int32, device=d))
+    _check(lib().hjcd_poccd_trace(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(seeds),
+                                  _ptr(out["theta"]), _ptr(out["cost"]), _ptr(out["ep"]), _ptr(out["eo"]),
+                                  _ptr(out["iters"]), _ptr(out["trace"]), _stream(stream)), "hjcd_poccd_trace")
     return out
 
 

@@ -140,5 +140,10 @@ def test_new_entry_points_validate_before_cuda(hjcd_lib):
     # the PO-CCD stop rule needs one cluster per target: M <= 2048
     big = hjcd_lib.default_config(M=3000)
     assert L.hjcd_poccd(r.handle, C.byref(big), fake, 1, None, fake, fake, None, None, None, None) == 2
+    assert L.hjcd_poccd_trace(r.handle, C.byref(big), fake, 1, None, fake, fake, None, None, None, fake,
+                              None) == 2
+    # the decision trace needs its buffer
+    assert L.hjcd_poccd_trace(r.handle, C.byref(c), fake, 1, None, fake, fake, None, None, None, None,
+                              None) == 1
     ok = hjcd_lib.default_config(M=3000, ccd_early_exit=0)
     assert L.hjcd_workspace_size(r.handle, 10, C.byref(ok), C.byref(n32)) == 0

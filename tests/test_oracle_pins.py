@@ -470,6 +470,40 @@ def test_poccd_target_early_exit_is_lockstep_truncation():
                 assert np.any((ex["ep"][t] < 5e-3) & (ex["eo"][t] < 5e-2))
 
 
+def test_poccd_replay_of_own_decisions_is_exact():
+    # decision replay (the GPU parity harness): replaying the oracle's own
+    # recorded decisions reproduces its run bit for bit with zero gaps, in both
+    # stop-rule modes; a flipped gamma decision or a non-argmin joint shows up
+    # as a positive gap and a different trajectory
+    ch = inputs.panda()
+    tg = oracle.fk(ch, inputs.halton_configs(ch, 3, start=11)).astype(np.float32)
+    for early in (0, 1):
+        p = params(M=40, ccd_early_exit=early, ccd_iters=20)
+        ref = oracle.po_ccd(ch, p, tg, trace=True)
+        rep = oracle.po_ccd_replay(ch, p, tg, ref["trace"], ref["iters"])
+        assert np.array_equal(rep["theta"], ref["theta"])
+        assert np.array_equal(rep["ep"], ref["ep"]) and np.array_equal(rep["eo"], ref["eo"])
+        assert rep["gap"].max() == 0.0 and rep["stop_gap"].max() == 0.0
+        w = ref["trace"][:, :, 0]
+        assert np.all((w & 31) < ch.dof) and np.all(((w >> 5) & 31) < ch.dof)
+        assert np.all(w >> 16 == 0) and np.all((w >> 12) & 3 != 3) and np.all((w >> 14) & 3 != 3)
+    # flip the first gamma decision of seed (0, 0)
+    bad = ref["trace"].copy()
+    assert ref["iters"][0, 0] > 0
+    bad[0, 0, 0] ^= 1 << 11
+    rep = oracle.po_ccd_replay(ch, p, tg, bad, ref["iters"])
+    assert rep["gap"][0, 0] > 0 and not np.array_equal(rep["theta"][0, :, 0], ref["theta"][0, :, 0])
+    assert rep["gap"][0, 1:].max() == 0.0
+    # force a different position joint: it scores worse than the argmin
+    bad = ref["trace"].copy()
+    bad[0, 1, 0] = (bad[0, 1, 0] & ~np.uint32(31)) | np.uint32(((bad[0, 1, 0] & 31) + 3) % ch.dof)
+    rep = oracle.po_ccd_replay(ch, p, tg, bad, ref["iters"])
+    assert rep["gap"][0, 1] > 0
+    # an out-of-range joint index is reported as an infinite gap
+    bad[0, 2, 0] = 31
+    assert np.isinf(oracle.po_ccd_replay(ch, p, tg, bad, ref["iters"])["gap"][0, 2])
+
+
 # ---------------------------------------------------------------- classic CCD (Alg. 1)
 def _planar_fk(L1, L2, th):
     x1 = np.array([L1 * math.cos(th[0]), L1 * math.sin(th[0])])
