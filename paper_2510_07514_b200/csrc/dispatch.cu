@@ -8,59 +8,60 @@ namespace hjcd {
 
 cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                          const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                         int32_t* iters, cudaStream_t s, uint32_t* trace) {
+                         int32_t* iters, cudaStream_t s, uint32_t* trace, uint32_t* ready) {
     switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
-        case 7: return launch_poccd_t<7, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
-        case 8: return launch_poccd_t<8, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
-        case 12: return launch_poccd_t<12, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
-        case 14: return launch_poccd_t<14, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
-        case 18: return launch_poccd_t<18, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
-        case 24: return launch_poccd_t<24, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
+        case 7: return launch_poccd_t<7, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
+        case 8: return launch_poccd_t<8, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
+        case 12: return launch_poccd_t<12, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
+        case 14: return launch_poccd_t<14, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
+        case 18: return launch_poccd_t<18, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
+        case 24: return launch_poccd_t<24, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
         default: break;
     }
-    if (rb.n <= 8) return launch_poccd_t<8, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
-    if (rb.n <= 16) return launch_poccd_t<16, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
-    return launch_poccd_t<32, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
+    if (rb.n <= 8) return launch_poccd_t<8, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
+    if (rb.n <= 16) return launch_poccd_t<16, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
+    return launch_poccd_t<32, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
 }
 
 template <class T>
 cudaError_t launch_pjik_coop(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
                              const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
-                             cudaStream_t s) {
+                             cudaStream_t s, const StageLink& link) {
     if (c.copies * c.K > 256 || 2 * c.A + 2 > 64) return cudaErrorInvalidConfiguration;
     switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
-        case 7: return launch_coop_t<T, 7, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
-        case 8: return launch_coop_t<T, 8, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
-        case 14: return launch_coop_t<T, 14, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+        case 7: return launch_coop_t<T, 7, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
+        case 8: return launch_coop_t<T, 8, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
+        case 14: return launch_coop_t<T, 14, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
         default: break;
     }
     if constexpr (sizeof(T) == 4) {   // Table II DoFs (fp32 polish only)
         switch (rb.n) {
-            case 12: return launch_coop_t<T, 12, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
-            case 18: return launch_coop_t<T, 18, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
-            case 24: return launch_coop_t<T, 24, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+            case 12: return launch_coop_t<T, 12, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
+            case 18: return launch_coop_t<T, 18, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
+            case 24: return launch_coop_t<T, 24, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
             default: break;
         }
     }
-    if (rb.n <= 8) return launch_coop_t<T, 8, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
-    if (rb.n <= 16) return launch_coop_t<T, 16, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
-    return launch_coop_t<T, 32, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+    if (rb.n <= 8) return launch_coop_t<T, 8, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
+    if (rb.n <= 16) return launch_coop_t<T, 16, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
+    return launch_coop_t<T, 32, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
 }
 template cudaError_t launch_pjik_coop<float>(const DevRobotT<float>&, const DevCfg&, const float*, int, const float*,
-                                             float*, float*, float*, int32_t*, int32_t*, cudaStream_t);
+                                             float*, float*, float*, int32_t*, int32_t*, cudaStream_t,
+                                             const StageLink&);
 
 cudaError_t launch_pjik64(const DevRobotT<double>& rb, const DevCfg& c, const float* targets, int T,
                           const float* seeds, double* theta, double* ep, double* eo, int32_t* counts,
                           int32_t* iters, cudaStream_t s) {
-    return launch_pjik_coop<double>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+    return launch_pjik_coop<double>(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s, StageLink());
 }
 
 cudaError_t launch_pjik(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                         const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
-                        int32_t* iters, cudaStream_t s) {
+                        int32_t* iters, cudaStream_t s, const StageLink& link) {
     // one CTA per target, warp-cooperative cascade (pjik_coop.cuh), for both
     // the per-target stop rule and the per-seed break
-    return launch_pjik_coop(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s);
+    return launch_pjik_coop(rb, c, targets, T, seeds, theta, ep, eo, counts, iters, s, link);
 }
 
 cudaError_t launch_ccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* seeds,

@@ -216,7 +216,7 @@ hjcd_status check_poccd(const hjcd_config* c) {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-    size_t theta1, cost1, seeds2, ep2, eo2, total;
+    size_t theta1, cost1, seeds2, ep2, eo2, ready, total;
 };
 
 Layout layout(int dof, long long T, const hjcd_config* c) {
@@ -227,8 +227,65 @@ Layout layout(int dof, long long T, const hjcd_config* c) {
     L.seeds2 = off; off += align256((size_t)T * c->B * dof * sizeof(float));
     L.ep2 = off;    off += align256((size_t)T * c->B * sizeof(float));
     L.eo2 = off;    off += align256((size_t)T * c->B * sizeof(float));
+    L.ready = off;  off += align256((size_t)T * sizeof(uint32_t));   // K10 per-target PO-CCD completion counts
+#ifdef HJCD_PROBE
+    off += align256((size_t)((T + 63) & ~63) * 4 + 5 * (size_t)T * 8);
+#endif
     L.total = off;
     return L;
+}
+
+#ifdef HJCD_PROBE
+unsigned long long* g_probe = nullptr;
+int g_probe_T = 0;
+#endif
+
+// hjcd_solve's launch sequence without stage events (DESIGN K10): PO-CCD
+// (lockstep clusters) counts each target's finished CTAs into `ready`; PJ-IK is
+// its programmatic dependent and starts on a target as soon as that target's
+// stage 1 is done, doing top-K + replication in its prologue, so the polish
+// of early targets overlaps the tail of PO-CCD. Needs the per-target PO-CCD
+// stop rule (R12b, one cluster per target); the per-seed break uses the
+// staged sequence. `final` launches Alg. 2 l.10 (best-select or best-N).
+template <class Final>
+cudaError_t solve_linked(const hjcd_robot* r, const DevCfg& d, const float* targets, int T, const Layout& L,
+                         char* ws, cudaStream_t s, Final final) {
+    float* theta1 = (float*)(ws + L.theta1);
+    float* cost1 = (float*)(ws + L.cost1);
+    float* seeds2 = (float*)(ws + L.seeds2);
+    float* ep2 = (float*)(ws + L.ep2);
+    float* eo2 = (float*)(ws + L.eo2);
+    cudaError_t e;
+    if (!d.ccd_early_exit) {
+        if ((e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s)) !=
+                cudaSuccess ||
+            (e = launch_select_replicate(r->dev, d, cost1, theta1, T, seeds2, nullptr, s)) != cudaSuccess ||
+            (e = launch_pjik(r->dev, d, targets, T, seeds2, seeds2, ep2, eo2, nullptr, nullptr, s)) != cudaSuccess)
+            return e;
+        return final(seeds2, ep2, eo2);
+    }
+    StageLink link;
+    link.ready = (uint32_t*)(ws + L.ready);
+    link.cost = cost1;
+    link.theta = theta1;
+    int nt, CL;
+    texit_shape(d.M, nt, CL);
+    link.need = (uint32_t)CL;
+    link.Mpad = 2;
+    while (link.Mpad < d.M) link.Mpad <<= 1;
+#ifdef HJCD_PROBE
+    g_probe = (unsigned long long*)(link.ready + ((T + 63) & ~63));
+    g_probe_T = T;
+    if ((e = cudaMemsetAsync(g_probe, 0xff, (size_t)T * 8, s)) != cudaSuccess ||
+        (e = cudaMemsetAsync(g_probe + T, 0, 4 * (size_t)T * 8, s)) != cudaSuccess)
+        return e;
+#endif
+    if ((e = cudaMemsetAsync(link.ready, 0, (size_t)T * sizeof(uint32_t), s)) != cudaSuccess ||
+        (e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s, nullptr,
+                          link.ready)) != cudaSuccess ||
+        (e = launch_pjik(r->dev, d, targets, T, nullptr, seeds2, ep2, eo2, nullptr, nullptr, s, link)) != cudaSuccess)
+        return e;
+    return final(seeds2, ep2, eo2);
 }
 
 struct Layout64 {
@@ -255,6 +312,14 @@ size_t host_staging(int dof, long long T) {
 }  // namespace
 
 extern "C" {
+
+#ifdef HJCD_PROBE
+// A/B diagnostic build only: copies the last linked solve's [5][T] stamps
+int hjcd_debug_probe(unsigned long long* host, int T) {
+    if (!g_probe || T != g_probe_T) return -1;
+    return (int)cudaMemcpy(host, g_probe, 5 * (size_t)T * 8, cudaMemcpyDeviceToHost);
+}
+#endif
 
 hjcd_status hjcd_robot_create(const hjcd_joint* joints, int32_t num_joints, const double ee_xyz[3],
                               const double ee_quat_wxyz[4], hjcd_robot** out) {
@@ -351,6 +416,13 @@ hjcd_status hjcd_solve_timed(const hjcd_robot* r, const hjcd_config* c, const fl
     auto mark = [&](int i) -> cudaError_t {
         return (events && events[i]) ? cudaEventRecord((cudaEvent_t)events[i], s) : cudaSuccess;
     };
+    if (!events) {   // DESIGN K10: PJ-IK as a dependent launch of PO-CCD
+        e = solve_linked(r, d, targets, T, L, ws, s, [&](const float* th, const float* ep, const float* eo) {
+            return launch_select_best(r->dev, d, targets, T, th, ep, eo, q_out, pos_err, ori_err, status, s);
+        });
+        return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+    }
+    // stage events requested: the staged sequence, one kernel per stage
     if ((e = mark(0)) != cudaSuccess) return cuda_fail(e);
     // Alg. 2 l.1: PO-CCD over M seeds per target
     if ((e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s)) != cudaSuccess ||
@@ -386,20 +458,11 @@ hjcd_status hjcd_solve_batch(const hjcd_robot* r, const hjcd_config* c, const fl
     Layout L = layout(r->dof, T, c);
     if (workspace_bytes < L.total || ((uintptr_t)workspace & 255)) return HJCD_E_WORKSPACE;
     char* ws = (char*)workspace;
-    float* theta1 = (float*)(ws + L.theta1);
-    float* cost1 = (float*)(ws + L.cost1);
-    float* seeds2 = (float*)(ws + L.seeds2);
-    float* ep2 = (float*)(ws + L.ep2);
-    float* eo2 = (float*)(ws + L.eo2);
     cudaStream_t s = (cudaStream_t)stream;
-    cudaError_t e;
-    if ((e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s)) != cudaSuccess ||
-        (e = launch_select_replicate(r->dev, d, cost1, theta1, T, seeds2, nullptr, s)) != cudaSuccess ||
-        (e = launch_pjik(r->dev, d, targets, T, seeds2, seeds2, ep2, eo2, nullptr, nullptr, s)) != cudaSuccess ||
-        (e = launch_select_topn(r->dev, d, targets, T, seeds2, ep2, eo2, N, q_out, pos_err, ori_err, nullptr, status,
-                                s)) != cudaSuccess)
-        return cuda_fail(e);
-    return HJCD_OK;
+    cudaError_t e = solve_linked(r, d, targets, T, L, ws, s, [&](const float* th, const float* ep, const float* eo) {
+        return launch_select_topn(r->dev, d, targets, T, th, ep, eo, N, q_out, pos_err, ori_err, nullptr, status, s);
+    });
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
 }
 
 hjcd_status hjcd_workspace_size_f64(const hjcd_robot* r, int32_t T, const hjcd_config* c, size_t* bytes) {

@@ -49,6 +49,42 @@ struct DevCfg {
     int64_t tid_offset;
 };
 
+// Dependent launch of PJ-IK on PO-CCD inside hjcd_solve (K10). With
+// ready != nullptr the PO-CCD lockstep kernel adds 1 to ready[t] (release, gpu
+// scope) when a CTA of target t's cluster has written its seeds, and the PJ-IK
+// kernel, launched as a programmatic dependent (it may start while PO-CCD still
+// runs), waits in each CTA until ready[t] == need, then does Alg. 2 l.2-8 (top-K
+// + replicate) for its target itself from cost / theta before polishing.
+struct StageLink {
+    uint32_t* ready = nullptr;     // [T], zeroed before the PO-CCD launch
+    const float* cost = nullptr;   // stage-1 cost [T][M]
+    const float* theta = nullptr;  // stage-1 theta [T][n][M]
+    uint32_t need = 0;             // CTAs per PO-CCD cluster
+    int32_t Mpad = 0;              // M rounded up to a power of two >= 2
+};
+
+// seeds per CTA (nt) and CTAs per cluster (CL) of the PO-CCD lockstep launch:
+// 128-thread CTAs (32 for M < 128), up to 16 per cluster (non-portable size
+// above 8), so M <= 2048
+inline void texit_shape(int M, int& nt, int& CL) {
+    nt = M < 128 ? (M + 31) / 32 * 32 : 128;
+    CL = (M + nt - 1) / nt;
+}
+
+#ifdef HJCD_PROBE
+// A/B diagnostic build only: %globaltimer stamps of the K10 schedule, stored
+// after the readiness counts: [5][T] = PO-CCD first CTA start, last CTA end,
+// PJ-IK CTA start, end of its wait, CTA end (ns)
+__device__ __forceinline__ unsigned long long probe_now() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+    return v;
+}
+__device__ __forceinline__ unsigned long long* probe_base(uint32_t* ready, int T) {
+    return (unsigned long long*)(ready + ((T + 63) & ~63));
+}
+#endif
+
 // Philox purposes (R30)
 enum : uint32_t { P_INIT = 1, P_PERTURB = 2, P_REPL = 3, P_PJPERT = 4 };
 
@@ -57,21 +93,21 @@ enum : uint32_t { P_INIT = 1, P_PERTURB = 2, P_REPL = 3, P_PJPERT = 4 };
 template <int NMAX, bool EXACT>
 cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                            const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                           int32_t* iters, uint32_t* trace, cudaStream_t s);
+                           int32_t* iters, uint32_t* trace, uint32_t* ready, cudaStream_t s);
 template <int NMAX, bool EXACT>
 cudaError_t launch_ccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* seeds,
                          float* theta, float* ep, int32_t* iters, cudaStream_t s);
 template <class T, int NMAX, bool EXACT>
 cudaError_t launch_coop_t(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
                           const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
-                          cudaStream_t s);
+                          cudaStream_t s, const StageLink& link);
 
 // launchers (dispatch.cu, select.cu); all asynchronous on `s`
 cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, float* jac,
                       cudaStream_t s);
 cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                          const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                         int32_t* iters, cudaStream_t s, uint32_t* trace = nullptr);
+                         int32_t* iters, cudaStream_t s, uint32_t* trace = nullptr, uint32_t* ready = nullptr);
 cudaError_t launch_ccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* seeds,
                        float* theta, float* ep, int32_t* iters, cudaStream_t s);
 cudaError_t launch_select_replicate(const DevRobot& rb, const DevCfg& c, const float* cost,
@@ -79,11 +115,11 @@ cudaError_t launch_select_replicate(const DevRobot& rb, const DevCfg& c, const f
                                     cudaStream_t s);
 cudaError_t launch_pjik(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                         const float* seeds, float* theta, float* ep, float* eo, int32_t* counts,
-                        int32_t* iters, cudaStream_t s);
+                        int32_t* iters, cudaStream_t s, const StageLink& link = StageLink());
 template <class T>
 cudaError_t launch_pjik_coop(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
                              const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
-                             cudaStream_t s);
+                             cudaStream_t s, const StageLink& link);
 cudaError_t launch_select_topn(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* theta,
                                const float* ep_all, const float* eo_all, int N, float* q_out, float* pos_err,
                                float* ori_err, int32_t* idx, int32_t* status, cudaStream_t s);

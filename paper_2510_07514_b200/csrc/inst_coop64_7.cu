@@ -2,5 +2,5 @@
 #include "pjik_coop.cuh"
 
 namespace hjcd {
-template cudaError_t launch_coop_t<double, 7, true>(const DevRobotT<double>&, const DevCfg&, const float*, int, const float*, double*, double*, double*, int32_t*, int32_t*, cudaStream_t);
+template cudaError_t launch_coop_t<double, 7, true>(const DevRobotT<double>&, const DevCfg&, const float*, int, const float*, double*, double*, double*, int32_t*, int32_t*, cudaStream_t, const StageLink&);
 }  // namespace hjcd

@@ -2,5 +2,5 @@
 #include "pjik_coop.cuh"
 
 namespace hjcd {
-template cudaError_t launch_coop_t<float, 24, true>(const DevRobotT<float>&, const DevCfg&, const float*, int, const float*, float*, float*, float*, int32_t*, int32_t*, cudaStream_t);
+template cudaError_t launch_coop_t<float, 24, true>(const DevRobotT<float>&, const DevCfg&, const float*, int, const float*, float*, float*, float*, int32_t*, int32_t*, cudaStream_t, const StageLink&);
 }  // namespace hjcd

@@ -2,6 +2,6 @@
 #include "pjik_coop.cuh"
 
 namespace hjcd {
-template cudaError_t launch_coop_t<float, 8, true>(const DevRobotT<float>&, const DevCfg&, const float*, int, const float*, float*, float*, float*, int32_t*, int32_t*, cudaStream_t);
-template cudaError_t launch_coop_t<float, 8, false>(const DevRobotT<float>&, const DevCfg&, const float*, int, const float*, float*, float*, float*, int32_t*, int32_t*, cudaStream_t);
+template cudaError_t launch_coop_t<float, 8, true>(const DevRobotT<float>&, const DevCfg&, const float*, int, const float*, float*, float*, float*, int32_t*, int32_t*, cudaStream_t, const StageLink&);
+template cudaError_t launch_coop_t<float, 8, false>(const DevRobotT<float>&, const DevCfg&, const float*, int, const float*, float*, float*, float*, int32_t*, int32_t*, cudaStream_t, const StageLink&);
 }  // namespace hjcd

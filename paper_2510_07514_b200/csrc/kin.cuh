@@ -344,4 +344,57 @@ __device__ __forceinline__ void perturb(const DevRobotT<T>& rb, const DevCfg& c,
     }
 }
 
+// ---- Alg. 2 l.2-8: top-K + replicate, shared by k_select_replicate and the
+// PJ-IK prologue of hjcd_solve's dependent launch (DESIGN K10)
+
+// non-negative float -> order-preserving uint32 (NaN and negatives -> +inf)
+__device__ __forceinline__ uint32_t cost_bits(float x) {
+    if (!(x >= 0.f)) x = CUDART_INF_F;
+    return __float_as_uint(x);
+}
+
+// The M stage-1 costs of one target as 64-bit keys (cost bits << 32 | seed
+// index), bitonic-sorted ascending in shared memory by the whole CTA (Mpad =
+// M rounded up to a power of two >= 2): keys[r] is the r-th of the K rounds
+// of argmin-and-remove of Alg. 2 (R14; ties -> lower index).  The costs are
+// read through L2 (ld.global.cg), never a possibly stale L1 line: in
+// hjcd_solve they were written by a PO-CCD kernel that may still be running.
+__device__ __forceinline__ void sort_stage1_keys(const float* cost_t, int M, int Mpad, unsigned long long* keys) {
+    for (int i = threadIdx.x; i < Mpad; i += blockDim.x)
+        keys[i] = (i < M) ? (((unsigned long long)cost_bits(__ldcg(cost_t + i)) << 32) | (unsigned)i) : ~0ull;
+    __syncthreads();
+    for (int size = 2; size <= Mpad; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < (Mpad >> 1); i += blockDim.x) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = ((lo & size) == 0);
+                const unsigned long long a = keys[lo], b = keys[hi];
+                if ((a > b) == up) { keys[lo] = b; keys[hi] = a; }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Alg. 2 l.7-8 (R15): joints j0..j0+3 of polish seed b < floor(B/K) K of
+// target t: kept seed b mod K, copy b / K; copies > 0 (or every copy with
+// repl_noise_all) get N(0, sigma_rep^2) from Philox (tid, b, REPL, 0, j / 4),
+// clamped to the fp32 limits.  theta1 is stage 1's [T][n][M], read through L2.
+template <class R>
+__device__ __forceinline__ float replica_value(const R& rb, const DevCfg& c, const float* theta1,
+                                               const unsigned long long* keys, int t, int b, int j,
+                                               uint32_t tid) {
+    const int K = c.K, M = c.M;
+    const int rank = b % K, cp = b / K;
+    const int src = (int)(keys[rank] & 0xffffffffu);
+    float v = __ldcg(theta1 + ((long long)t * rb.n + j) * M + src);
+    if (cp > 0 || c.repl_noise_all) {
+        float g[4];
+        normals4(draw(c, tid, (uint32_t)b, P_REPL, 0u, (uint32_t)(j >> 2)), g);
+        v = clampf(__fmaf_rn(c.sigma_rep, g[j & 3], v), (float)rb.j[j].lo, (float)rb.j[j].hi);
+    }
+    return v;
+}
+
 }  // namespace hjcd

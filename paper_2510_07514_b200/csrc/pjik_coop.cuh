@@ -16,6 +16,8 @@
 // parallel.  Each failing seed then takes the FIRST successful trial in cascade
 // order (LM alpha_1..alpha_A, dogleg, single alpha_0..alpha_A) — exactly the
 // step the sequential cascade takes; extra evaluations have no side effects.
+#include <algorithm>
+
 #include "polish.cuh"
 
 namespace hjcd {
@@ -62,7 +64,7 @@ __global__ void __launch_bounds__(256)
 k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ DevCfg c,
             const float* __restrict__ targets, const float* __restrict__ seeds,
             T* __restrict__ theta_out, T* __restrict__ ep_out, T* __restrict__ eo_out,
-            int32_t* __restrict__ counts_out, int32_t* __restrict__ iters_out) {
+            int32_t* __restrict__ counts_out, int32_t* __restrict__ iters_out, const StageLink link) {
     extern __shared__ unsigned long long coop_raw[];
     __shared__ int s_wtot[8];   // per-warp item totals (<= 256 threads)
     __shared__ T s_alpha[32];   // line-search steps beta^-a, a = 0..A (A <= 31), by repeated products
@@ -83,8 +85,44 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
     }   // published by the first __syncthreads_or of the iteration loop
 
     T th[NMAX], tt[NMAX], dth[NMAX];
+    if (link.ready) {
+        // DESIGN K10 (hjcd_solve): wait until every CTA of this target's PO-CCD
+        // cluster has published its seeds (acquire, gpu scope), then Alg. 2
+        // l.2-8 for this target in this CTA: top-K keys sorted in the (not yet
+        // used) cascade shared memory, the B x n replicas staged after them
+#ifdef HJCD_PROBE
+        const int TT = (int)gridDim.x;
+        unsigned long long* pr = probe_base(link.ready, TT);
+        if (b == 0) pr[2 * TT + t] = probe_now();
+#endif
+        if (b == 0) {
+            const uint32_t* f = link.ready + t;
+            uint32_t v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                if (v >= link.need) break;
+                __nanosleep(500);
+            }
+        }
+        __syncthreads();
+#ifdef HJCD_PROBE
+        if (b == 0) pr[3 * TT + t] = probe_now();
+#endif
+        sort_stage1_keys(link.cost + (long long)t * c.M, c.M, link.Mpad, coop_raw);
+        float* stage = (float*)(coop_raw + link.Mpad);   // [used][NMAX]
+#pragma unroll 1
+        for (int e = b; e < used * n; e += nt) {
+            const int bb = e / n, j = e - bb * n;
+            stage[bb * NMAX + j] = replica_value(rb, c, link.theta, coop_raw, t, bb, j, tid);
+        }
+        __syncthreads();
 #pragma unroll
-    for (int j = 0; j < NMAX; ++j) th[j] = (active && (EXACT || j < n)) ? T(seeds[row * n + j]) : T(0);
+        for (int j = 0; j < NMAX; ++j) th[j] = (active && (EXACT || j < n)) ? T(stage[b * NMAX + j]) : T(0);
+        __syncthreads();   // the keys' shared memory becomes the cascade's
+    } else {
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) th[j] = (active && (EXACT || j < n)) ? T(seeds[row * n + j]) : T(0);
+    }
 
     int cnt[4] = {0, 0, 0, 0};
     vec3<T> Jp[NMAX], Jo[NMAX];
@@ -286,6 +324,9 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
         }
     }
 
+#ifdef HJCD_PROBE
+    if (link.ready && b == 0) probe_base(link.ready, (int)gridDim.x)[4 * gridDim.x + t] = probe_now();
+#endif
     if (!active) return;
 #pragma unroll
     for (int j = 0; j < NMAX; ++j)
@@ -302,30 +343,49 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
 template <class T, int NMAX, bool EXACT, bool REV>
 static cudaError_t launch_coop_r(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
                                  const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, const StageLink& link) {
     const int used = c.copies * c.K;
     const int block = (used + 31) / 32 * 32;
-    const size_t smem = coop_smem_bytes<T, NMAX>(block);
+    size_t smem = coop_smem_bytes<T, NMAX>(block);
+    if (link.ready)   // K10 top-K keys + replica staging
+        smem = std::max(smem, (size_t)link.Mpad * sizeof(unsigned long long) + (size_t)used * NMAX * sizeof(float));
     static bool attr = false;
     if (!attr) {
+        const size_t mx = std::max(coop_smem_bytes<T, NMAX>(256),
+                                   (size_t)8192 * sizeof(unsigned long long) + (size_t)256 * NMAX * sizeof(float));
         cudaError_t e = cudaFuncSetAttribute(k_pjik_coop<T, NMAX, EXACT, REV>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)coop_smem_bytes<T, NMAX>(256));
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_pjik_coop<T, NMAX, EXACT, REV><<<T_, block, smem, s>>>(rb, c, targets, seeds, theta, ep, eo, counts, iters);
-    return cudaGetLastError();
+    if (!link.ready) {
+        k_pjik_coop<T, NMAX, EXACT, REV><<<T_, block, smem, s>>>(rb, c, targets, seeds, theta, ep, eo, counts, iters,
+                                                                 link);
+        return cudaGetLastError();
+    }
+    // DESIGN K10: programmatic dependent of the PO-CCD launch before it on `s`
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)T_, 1, 1);
+    cfg.blockDim = dim3((unsigned)block, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr1[1];
+    attr1[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr1[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr1;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_pjik_coop<T, NMAX, EXACT, REV>, rb, c, targets, seeds, theta, ep, eo, counts,
+                              iters, link);
 }
 
 // all-revolute chains run the kernel without per-joint type branches
 template <class T, int NMAX, bool EXACT>
 cudaError_t launch_coop_t(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
                           const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
-                          cudaStream_t s) {
+                          cudaStream_t s, const StageLink& link) {
     if (rb.pmask == 0u)
-        return launch_coop_r<T, NMAX, EXACT, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
-    return launch_coop_r<T, NMAX, EXACT, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s);
+        return launch_coop_r<T, NMAX, EXACT, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
+    return launch_coop_r<T, NMAX, EXACT, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
 }
 
 }  // namespace hjcd

@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(128, poccd_min_blocks<NMAX>())
 k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float* __restrict__ targets, int T, const float* __restrict__ seeds,
         float* __restrict__ theta_out, float* __restrict__ cost_out, float* __restrict__ ep_out,
-        float* __restrict__ eo_out, int32_t* __restrict__ iters_out, int CL, uint32_t* __restrict__ trace) {
+        float* __restrict__ eo_out, int32_t* __restrict__ iters_out, int CL, uint32_t* __restrict__ trace,
+        uint32_t* __restrict__ ready) {
     const int M = c.M;
     const int n = rb.n;
     int t, m;
@@ -54,6 +55,13 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         t = (int)(blockIdx.x / (unsigned)CL);
         m = (int)(blockIdx.x - (unsigned)t * CL) * (int)blockDim.x + (int)threadIdx.x;
         active = m < M;
+        // DESIGN K10: the dependent PJ-IK grid may be scheduled once every CTA
+        // of this grid is resident or done, so its waiting CTAs never hold
+        // resources a PO-CCD CTA still needs
+        if (ready) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef HJCD_PROBE
+        if (ready && threadIdx.x == 0) atomicMin(probe_base(ready, T) + t, probe_now());
+#endif
         if (threadIdx.x < 3) s_flag[threadIdx.x] = 0;
         cg::this_cluster().sync();   // flags initialised before any remote store
     } else {
@@ -291,15 +299,24 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         }
     }
 
-    if (!active) return;
+    if (active) {
 #pragma unroll
-    for (int j = 0; j < NMAX; ++j)
-        if (EXACT || j < n) theta_out[((long long)t * n + j) * M + m] = th[j];
-    const long long o = (long long)t * M + m;
-    cost_out[o] = c.w_p * c.w_p * ep * ep + c.w_o * c.w_o * eo * eo;   // R14
-    if (ep_out) ep_out[o] = ep;
-    if (eo_out) eo_out[o] = eo;
-    if (iters_out) iters_out[o] = k;
+        for (int j = 0; j < NMAX; ++j)
+            if (EXACT || j < n) theta_out[((long long)t * n + j) * M + m] = th[j];
+        const long long o = (long long)t * M + m;
+        cost_out[o] = c.w_p * c.w_p * ep * ep + c.w_o * c.w_o * eo * eo;   // R14
+        if (ep_out) ep_out[o] = ep;
+        if (eo_out) eo_out[o] = eo;
+        if (iters_out) iters_out[o] = k;
+    }
+    if (TEXIT && ready) {   // DESIGN K10: this CTA's seeds of target t are in memory
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(ready + t, 1u);
+#ifdef HJCD_PROBE
+        if (threadIdx.x == 0) atomicMax(probe_base(ready, T) + T + t, probe_now());
+#endif
+    }
 }
 
 template <int NMAX>
@@ -307,18 +324,10 @@ inline size_t poccd_smem(int nt) {   // the per-thread frames (24 B per joint) f
     return NMAX <= 18 ? (size_t)NMAX * nt * (sizeof(float4) + sizeof(float2)) : 0;
 }
 
-// seeds per CTA (nt) and CTAs per cluster (CL) of the lockstep launch:
-// 128-thread CTAs (32 for M < 128), up to 16 per cluster (non-portable size
-// above 8), so M <= 2048
-static inline void texit_shape(int M, int& nt, int& CL) {
-    nt = M < 128 ? (M + 31) / 32 * 32 : 128;
-    CL = (M + nt - 1) / nt;
-}
-
 template <int NMAX, bool EXACT, bool REV>
 static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                   const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                                  int32_t* iters, uint32_t* trace, cudaStream_t s) {
+                                  int32_t* iters, uint32_t* trace, uint32_t* ready, cudaStream_t s) {
     static bool smem_attr = false;   // NMAX = 16: the frames copy is 48 KB, above the default limit
     if (!smem_attr && poccd_smem<NMAX>(128) > 0) {
         cudaError_t e;
@@ -335,7 +344,7 @@ static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const flo
         const long long grid = (total + block - 1) / block;
         if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
         k_poccd<NMAX, EXACT, false, REV><<<(unsigned)grid, block, poccd_smem<NMAX>(block), s>>>(
-            rb, c, targets, T, seeds, theta, cost, ep, eo, iters, 1, trace);
+            rb, c, targets, T, seeds, theta, cost, ep, eo, iters, 1, trace, nullptr);
         return cudaGetLastError();
     }
     int nt, CL;
@@ -365,17 +374,17 @@ static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const flo
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k_poccd<NMAX, EXACT, true, REV>, rb, c, targets, T, seeds, theta, cost, ep, eo,
-                              iters, CL, trace);
+                              iters, CL, trace, ready);
 }
 
 // all-revolute chains (the usual case) run the kernels without per-joint type branches
 template <int NMAX, bool EXACT>
 cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                            const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                           int32_t* iters, uint32_t* trace, cudaStream_t s) {
+                           int32_t* iters, uint32_t* trace, uint32_t* ready, cudaStream_t s) {
     if (rb.pmask == 0u)
-        return launch_poccd_r<NMAX, EXACT, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
-    return launch_poccd_r<NMAX, EXACT, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, s);
+        return launch_poccd_r<NMAX, EXACT, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
+    return launch_poccd_r<NMAX, EXACT, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
 }
 
 }  // namespace hjcd

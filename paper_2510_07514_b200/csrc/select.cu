@@ -12,57 +12,21 @@
 
 namespace hjcd {
 
-// non-negative float -> order-preserving uint32 (NaN and negatives -> +inf)
-__device__ __forceinline__ uint32_t cost_bits(float x) {
-    if (!(x >= 0.f)) x = CUDART_INF_F;
-    return __float_as_uint(x);
-}
-
 __global__ void __launch_bounds__(512)
 k_select_replicate(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
                    const float* __restrict__ cost, const float* __restrict__ theta, int Mpad,
                    float* __restrict__ seeds, int32_t* __restrict__ kept) {
     extern __shared__ unsigned long long keys[];
     const int t = blockIdx.x;
-    const int M = c.M, K = c.K, B = c.B, n = rb.n;
-    const float* ct = cost + (long long)t * M;
-    for (int i = threadIdx.x; i < Mpad; i += blockDim.x)
-        keys[i] = (i < M) ? (((unsigned long long)cost_bits(__ldg(ct + i)) << 32) | (unsigned)i)
-                          : ~0ull;
-    __syncthreads();
-    // bitonic sort, ascending
-    for (int size = 2; size <= Mpad; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = threadIdx.x; i < (Mpad >> 1); i += blockDim.x) {
-                const int lo = 2 * i - (i & (stride - 1));
-                const int hi = lo + stride;
-                const bool up = ((lo & size) == 0);
-                const unsigned long long a = keys[lo], b = keys[hi];
-                if ((a > b) == up) { keys[lo] = b; keys[hi] = a; }
-            }
-            __syncthreads();
-        }
-    }
+    const int K = c.K, B = c.B, n = rb.n;
+    sort_stage1_keys(cost + (long long)t * c.M, c.M, Mpad, keys);
     if (kept)
         for (int r = threadIdx.x; r < K; r += blockDim.x) kept[(long long)t * K + r] = (int32_t)(keys[r] & 0xffffffffu);
     const uint32_t tid = (uint32_t)(c.tid_offset + t);
     const int used = c.copies * K;
     for (int e = threadIdx.x; e < B * n; e += blockDim.x) {
         const int b = e / n, j = e - b * n;
-        float v;
-        if (b >= used) {
-            v = CUDART_NAN_F;
-        } else {
-            const int rank = b % K, cp = b / K;
-            const int src = (int)(keys[rank] & 0xffffffffu);
-            v = theta[((long long)t * n + j) * M + src];
-            if (cp > 0 || c.repl_noise_all) {
-                float g[4];
-                normals4(draw(c, tid, (uint32_t)b, P_REPL, 0u, (uint32_t)(j >> 2)), g);
-                v = clampf(v + c.sigma_rep * g[j & 3], rb.j[j].lo, rb.j[j].hi);
-            }
-        }
-        seeds[((long long)t * B + b) * n + j] = v;
+        seeds[((long long)t * B + b) * n + j] = b < used ? replica_value(rb, c, theta, keys, t, b, j, tid) : CUDART_NAN_F;
     }
 }
 

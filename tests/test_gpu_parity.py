@@ -584,3 +584,35 @@ def test_solve_other_chains(hjcd_lib, cuda, name):
     assert success(pe64, oe64).mean() >= 0.95
     rq, rpe, roe, rst = oracle.solve(ch, p, tg[:8])
     assert abs(success(pe64[:8], oe64[:8]).mean() - success(rpe, roe).mean()) <= 1 / 8 + 1e-9
+
+
+@pytest.mark.parametrize("name,M,Tn,early", [("panda", 1000, 300, 1), ("fetch", 64, 50, 1),
+                                             ("panda_x24", 2000, 20, 1), ("panda", 256, 40, 0)])
+def test_solve_dependent_launch_equals_staged(hjcd_lib, cuda, name, M, Tn, early):
+    """DESIGN K10: hjcd_solve without stage events launches PJ-IK as a dependent
+    of PO-CCD (per-target readiness counts, top-K + replication in the PJ-IK
+    prologue); with events it runs one kernel per stage. Both must give the
+    same bytes, and solve_batch must equal the staged entry points."""
+    import torch
+    ch = inputs.robot(name)
+    rb = hjcd_lib.Robot(ch)
+    tg, _ = targets_for(ch, Tn, start=77)
+    p = params(M=M, K=min(50, M), B=100, ccd_early_exit=early)
+    cfg = hjcd_lib.config_from_params(p)
+    tgd = T(tg, cuda)
+    for _ in range(2):   # the second call reuses the workspace (readiness counts re-zeroed)
+        ws = hjcd_lib.Workspace()
+        fused = hjcd_lib.solve(rb, tgd, cfg, workspace=ws)
+        fused2 = hjcd_lib.solve(rb, tgd, cfg, workspace=ws)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        staged = hjcd_lib.solve(rb, tgd, cfg, events=evs)
+        torch.cuda.synchronize()
+        for a, b, c in zip(fused, fused2, staged):
+            assert torch.equal(a, b) and torch.equal(a, c)
+    o1 = hjcd_lib.poccd(rb, cfg, tgd)
+    seeds, _ = hjcd_lib.select_replicate(rb, cfg, o1["cost"], o1["theta"])
+    o2 = hjcd_lib.pjik(rb, cfg, tgd, seeds)
+    q, pe, oe, idx = hjcd_lib.select_topn(rb, cfg, tgd, o2["theta"], o2["ep"], o2["eo"], 10)
+    qb, peb, oeb, stb = hjcd_lib.solve_batch(rb, tgd, 10, cfg)
+    assert torch.equal(q, qb) and torch.equal(pe, peb) and torch.equal(oe, oeb)
+    assert torch.equal(stb, staged[3])
