@@ -173,7 +173,9 @@ hjcd_status hjcd_solve_batch(const hjcd_robot* r, const hjcd_config* c, const fl
  * and best-select in fp64 on an fp64 copy of the chain, so the fine tolerances
  * can go to SPEC's 1e-9 m / 1e-8 rad.  Outputs are fp64: q_out [T][dof],
  * pos_err/ori_err [T] (device); status [T] as hjcd_solve.  Workspace: device,
- * >= hjcd_workspace_size_f64 bytes, 256-byte aligned. */
+ * >= hjcd_workspace_size_f64 bytes, 256-byte aligned.  The fp64 polish keeps
+ * per-seed records in shared memory: with dof > 16, floor(B/K)*K <= 160
+ * (227 KB per CTA), otherwise HJCD_E_CUDA ("invalid configuration"). */
 hjcd_status hjcd_workspace_size_f64(const hjcd_robot* r, int32_t T, const hjcd_config* c, size_t* bytes);
 hjcd_status hjcd_solve_f64(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
                            double* q_out, double* pos_err, double* ori_err, int32_t* status,

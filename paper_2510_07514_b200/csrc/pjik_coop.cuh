@@ -349,14 +349,15 @@ static cudaError_t launch_coop_r(const DevRobotT<T>& rb, const DevCfg& c, const 
     size_t smem = coop_smem_bytes<T, NMAX>(block);
     if (link.ready)   // K10 top-K keys + replica staging
         smem = std::max(smem, (size_t)link.Mpad * sizeof(unsigned long long) + (size_t)used * NMAX * sizeof(float));
-    static bool attr = false;
-    if (!attr) {
-        const size_t mx = std::max(coop_smem_bytes<T, NMAX>(256),
-                                   (size_t)8192 * sizeof(unsigned long long) + (size_t)256 * NMAX * sizeof(float));
+    // opt in to what this launch needs (the fp64 records at NMAX = 32 exceed the
+    // 227 KB per-CTA limit above 160 polish seeds: a clean configuration error)
+    if (smem > (size_t)227 * 1024) return cudaErrorInvalidConfiguration;
+    static size_t attr = 48 * 1024;
+    if (smem > attr) {
         cudaError_t e = cudaFuncSetAttribute(k_pjik_coop<T, NMAX, EXACT, REV>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr = smem;
     }
     if (!link.ready) {
         k_pjik_coop<T, NMAX, EXACT, REV><<<T_, block, smem, s>>>(rb, c, targets, seeds, theta, ep, eo, counts, iters,

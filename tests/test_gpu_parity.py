@@ -616,3 +616,17 @@ def test_solve_dependent_launch_equals_staged(hjcd_lib, cuda, name, M, Tn, early
     qb, peb, oeb, stb = hjcd_lib.solve_batch(rb, tgd, 10, cfg)
     assert torch.equal(q, qb) and torch.equal(pe, peb) and torch.equal(oe, oeb)
     assert torch.equal(stb, staged[3])
+
+
+def test_solve_f64_high_dof(hjcd_lib, cuda):
+    """fp64 polish at n = 24 (NMAX = 32 records): the kernel opts in to the
+    shared memory it needs; beyond 227 KB per CTA it fails cleanly."""
+    ch = inputs.robot("panda_x24")
+    rb = hjcd_lib.Robot(ch)
+    tg, _ = targets_for(ch, 4)
+    p = params(M=256, K=16, B=128, lm_iters=64)
+    q, pe, oe, st = hjcd_lib.solve_f64(rb, T(tg, cuda), hjcd_lib.config_from_params(p))
+    pe64, oe64 = fp64_errors(ch, N(q), tg)
+    assert np.abs(pe64 - N(pe)).max() < 1e-10 and success(pe64, oe64).all()
+    with pytest.raises(hjcd_lib.HjcdError):
+        hjcd_lib.solve_f64(rb, T(tg, cuda), hjcd_lib.config_from_params(params(M=256, K=16, B=192)))
