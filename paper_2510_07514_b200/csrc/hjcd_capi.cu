@@ -168,6 +168,16 @@ hjcd_status build_robot(const hjcd_joint* joints, int32_t num, const double ee_x
         acc = rt_transpose_rot(C);
         d++;
     }
+    // K11: the DH-twist pattern F_j.R = Rx(alpha_j), tested on the stored values
+#ifndef HJCD_NO_RX   // (A/B builds only)
+    r->dev.rx = r->dev64.rx = 1u;
+#endif
+    for (int k = 0; k < dof; ++k) {
+        const float* R = r->dev.j[k].R;
+        const double* R64 = r->dev64.j[k].R;
+        if (!(R[0] == 1.f && R[1] == 0.f && R[2] == 0.f && R[3] == 0.f && R[6] == 0.f)) r->dev.rx = 0u;
+        if (!(R64[0] == 1.0 && R64[1] == 0.0 && R64[2] == 0.0 && R64[3] == 0.0 && R64[6] == 0.0)) r->dev64.rx = 0u;
+    }
     Rt E = rt_mul(acc, rt_from_pose(ee_xyz, ee_quat));
     store(E, r->dev.eeR, r->dev.eet);
     store(E, r->dev64.eeR, r->dev64.eet);

@@ -30,7 +30,9 @@ template <class S>
 struct DevRobotT {
     int32_t n;
     uint32_t pmask;      // bit j set: DoF joint j is prismatic
-    int32_t pad[2];
+    uint32_t rx;         // 1: every DoF joint's F_j rotation is Rx(alpha) (DH twist; R[0] = 1,
+                         //    R[1] = R[2] = R[3] = R[6] = 0 exactly in this precision): DESIGN K11
+    int32_t pad;
     DevJointT<S> j[HJCD_MAX_DOF];
     S eeR[9];
     S eet[3];

@@ -149,8 +149,11 @@ __device__ __forceinline__ void sincos_b(double x, double* s, double* c) { sinco
 // EXACT: the chain has exactly NMAX DoF (no per-joint guard).  FAST: joint
 // sincos on the SFU (__sincosf, |err| <~ 5e-7 rad on the joint ranges): used by
 // the coarse stage only (K5); the polish stage uses sincos_b.
-// REV: every DoF joint is revolute (no per-joint type branch).
-template <int NMAX, bool FRAMES, bool EXACT = false, bool FAST = false, bool REV = false, class T>
+// REV: 1 = every DoF joint is revolute (no per-joint type branch); 2 = also
+// every F_j rotation is Rx(alpha_j) (rb.rx, DESIGN K11): the rotation product
+// skips the structural zeros (12 instead of 27 multiply-adds per joint) with
+// the same operation order on the non-zero terms, i.e. the same bits.
+template <int NMAX, bool FRAMES, bool EXACT = false, bool FAST = false, int REV = 0, class T>
 __device__ __forceinline__ void fk(const DevRobotT<T>& rb, const T (&th)[NMAX], vec3<T> (&P)[NMAX],
                                    vec3<T> (&Z)[NMAX], vec3<T>& pe, QuatT<T>& qe) {
     T R[9] = {T(1), T(0), T(0), T(0), T(1), T(0), T(0), T(0), T(1)};
@@ -163,11 +166,20 @@ __device__ __forceinline__ void fk(const DevRobotT<T>& rb, const T (&th)[NMAX], 
             ty += R[3] * J.t[0] + R[4] * J.t[1] + R[5] * J.t[2];
             tz += R[6] * J.t[0] + R[7] * J.t[1] + R[8] * J.t[2];
             T N[9];
+            if constexpr (REV == 2) {
 #pragma unroll
-            for (int r = 0; r < 3; ++r)
+                for (int r = 0; r < 3; ++r) {
+                    N[3 * r] = R[3 * r];
+                    N[3 * r + 1] = R[3 * r + 1] * J.R[4] + R[3 * r + 2] * J.R[7];
+                    N[3 * r + 2] = R[3 * r + 1] * J.R[5] + R[3 * r + 2] * J.R[8];
+                }
+            } else {
 #pragma unroll
-                for (int cc = 0; cc < 3; ++cc)
-                    N[3 * r + cc] = R[3 * r] * J.R[cc] + R[3 * r + 1] * J.R[3 + cc] + R[3 * r + 2] * J.R[6 + cc];
+                for (int r = 0; r < 3; ++r)
+#pragma unroll
+                    for (int cc = 0; cc < 3; ++cc)
+                        N[3 * r + cc] = R[3 * r] * J.R[cc] + R[3 * r + 1] * J.R[3 + cc] + R[3 * r + 2] * J.R[6 + cc];
+            }
             if (FRAMES) {
                 P[j] = mk3<T>(tx, ty, tz);
                 Z[j] = mk3<T>(N[2], N[5], N[8]);

@@ -59,7 +59,7 @@ size_t coop_smem_bytes(int nt) {
 }
 
 // REV: every DoF joint is revolute (no per-joint type branches)
-template <class T, int NMAX, bool EXACT, bool REV>
+template <class T, int NMAX, bool EXACT, int REV>
 __global__ void __launch_bounds__(256)
 k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ DevCfg c,
             const float* __restrict__ targets, const float* __restrict__ seeds,
@@ -130,6 +130,14 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
     bool live = active;   // per-seed mode: cleared when this seed converges
     int kseed = 0;
     int k;
+#ifdef HJCD_PROBE2
+    // A/B diagnostic build only: thread 0's cycles per iteration segment
+    long long p2_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, p2_last = clock64();
+    int p2_items = 0;
+#define P2MARK(i) do { if (b == 0) { const long long nw = clock64(); p2_acc[i] += nw - p2_last; p2_last = nw; } } while (0)
+#else
+#define P2MARK(i) do {} while (0)
+#endif
     for (k = 0;; ++k) {
         vec3<T> pe;
         QuatT<T> qe;
@@ -147,6 +155,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
             if (conv) { live = false; kseed = k; }
             if (!__syncthreads_or(live)) break;
         }
+        P2MARK(0);
         if (k == c.lm_iters) break;
 
         bool need = false, have_lm = false, accepted = false;
@@ -183,6 +192,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
             c0 = cost_w(W, r.rho);
             have_lm = lm_direction<NMAX, EXACT>(rb, c, Jp, Jo, invD, W, r.rho, dth);
         }
+        P2MARK(1);
 
         // ---- trial evaluation, ONE site in two phases (K6).  Phase 0: every
         // live seed evaluates its own LM trial at alpha = 1 (Alg. 4 l.3-9, the
@@ -232,11 +242,15 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                 if (lane == 31) s_wtot[b >> 5] = incl;
                 S.ok[b] = 0ull;
                 __syncthreads();
+                P2MARK(3);
                 for (int w = 0; w < (nt >> 5); ++w) {
                     const int v = s_wtot[w];
                     if (w < (b >> 5)) incl += v;
                     total += v;
                 }
+#ifdef HJCD_PROBE2
+                p2_items += total;
+#endif
                 if (total == 0) break;   // uniform over the CTA
                 // item -> (owner, index) table: each failing seed fills its range
                 for (int i = 0; i < items; ++i) {
@@ -244,6 +258,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                     S.ownq[incl - items + i] = (unsigned char)i;
                 }
                 __syncthreads();
+                P2MARK(4);
             }
             bool own_ok = false;
             for (int it = b;; it += nt) {
@@ -294,6 +309,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                 }
             }
             if (phase == 0) {
+                P2MARK(2);
                 if (own_ok) {
                     accepted = true;
                     cnt[0]++;
@@ -303,6 +319,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                 continue;
             }
             __syncthreads();
+            P2MARK(5);
             if (need) {
                 const unsigned long long m = S.ok[b];
                 if (m) {
@@ -322,7 +339,9 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                 }
             }
         }
+        P2MARK(6);
     }
+#undef P2MARK
 
 #ifdef HJCD_PROBE
     if (link.ready && b == 0) probe_base(link.ready, (int)gridDim.x)[4 * gridDim.x + t] = probe_now();
@@ -338,9 +357,15 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
         for (int i = 0; i < 4; ++i) counts_out[row * 4 + i] = cnt[i];
     }
     if (iters_out) iters_out[row] = (c.target_early_exit || live) ? k : kseed;
+#ifdef HJCD_PROBE2
+    if (b == 0 && counts_out) {   // overwrite seeds 0-1's step counts with the segment totals
+        for (int i = 0; i < 7; ++i) counts_out[(long long)t * c.B * 4 + i] = (int32_t)(p2_acc[i] >> 4);
+        counts_out[(long long)t * c.B * 4 + 7] = p2_items;
+    }
+#endif
 }
 
-template <class T, int NMAX, bool EXACT, bool REV>
+template <class T, int NMAX, bool EXACT, int REV>
 static cudaError_t launch_coop_r(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
                                  const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
                                  cudaStream_t s, const StageLink& link) {
@@ -384,9 +409,11 @@ template <class T, int NMAX, bool EXACT>
 cudaError_t launch_coop_t(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
                           const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
                           cudaStream_t s, const StageLink& link) {
+    if (rb.pmask == 0u && rb.rx)
+        return launch_coop_r<T, NMAX, EXACT, 2>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
     if (rb.pmask == 0u)
-        return launch_coop_r<T, NMAX, EXACT, true>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
-    return launch_coop_r<T, NMAX, EXACT, false>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
+        return launch_coop_r<T, NMAX, EXACT, 1>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
+    return launch_coop_r<T, NMAX, EXACT, 0>(rb, c, targets, T_, seeds, theta, ep, eo, counts, iters, s, link);
 }
 
 }  // namespace hjcd

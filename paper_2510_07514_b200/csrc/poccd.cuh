@@ -35,7 +35,7 @@ namespace hjcd {
 template <int NMAX>
 constexpr int poccd_min_blocks() { return NMAX <= 14 ? 4 : (NMAX <= 18 ? 3 : 2); }
 
-template <int NMAX, bool EXACT, bool TEXIT, bool REV>
+template <int NMAX, bool EXACT, bool TEXIT, int REV>
 __global__ void __launch_bounds__(128, poccd_min_blocks<NMAX>())
 k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float* __restrict__ targets, int T, const float* __restrict__ seeds,
@@ -145,12 +145,14 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float3 vq = f3(qr.x, qr.y, qr.z);
         const float dphi = phi > 0.f ? fmaxf(c.delta_min, c.delta0 * rho_k) * phi : 0.f;   // delta(k) phi
         const float tau2 = c.tau_deg * c.tau_deg;
-        // K2b: for an unclamped orientation candidate d = sgn(v.z) dphi,
-        //   |v'|^2 = C^2 |v|^2 + S^2 (w^2 + |v|^2 - (v.z)^2) - 2 C S w |v.z|,
-        // C, S = cos, sin(dphi / 2) shared by all joints (expand q_err (x) q(z, -d))
+        // K2b: for an orientation candidate d, expanding q_err (x) q(z, -d) gives
+        //   |v'|^2 = C^2 |v|^2 + S^2 (w^2 + |v|^2 - (v.z)^2) - 2 C S w (v.z),
+        // C, S = cos, sin(d / 2).  Unclamped, d = sgn(v.z) dphi: C, S of dphi / 2
+        // are shared by all joints and the last term is -2 C S w |v.z|.
         float Cd, Sd;
         __sincosf(0.5f * dphi, &Sd, &Cd);
-        const float ob0 = Cd * Cd * (sv * sv) + Sd * Sd * (qr.w * qr.w + sv * sv);
+        const float sv2 = sv * sv, wsv2 = qr.w * qr.w + sv2;
+        const float ob0 = Cd * Cd * sv2 + Sd * Sd * wsv2;
         const float ob1 = Sd * Sd, ob2 = 2.f * Cd * Sd * qr.w;
 
         // ---- Alg. 3 l.6-9: per-joint candidates, scored, greedy argmin
@@ -194,10 +196,9 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
                     } else if (tsum >= J.lo && tsum <= J.hi) {
                         const float avz = fabsf(vz);
                         so = ob0 - avz * fmaf(ob1, avz, ob2);   // K2b closed form
-                    } else {                              // clamped step: rotate by the effective d
-                        __sincosf(0.5f * dor, &s2, &c2);
-                        const Quat q2 = qerr_rotate(qr, z, c2, s2);
-                        so = q2.x * q2.x + q2.y * q2.y + q2.z * q2.z;
+                    } else {                              // clamped step: the same closed form at
+                        __sincosf(0.5f * dor, &s2, &c2);  // the effective d (C, S of d / 2, signed)
+                        so = c2 * c2 * sv2 + s2 * s2 * (wsv2 - vz * vz) - 2.f * c2 * s2 * qr.w * vz;
                     }
                 } else {
                     // prismatic (R32): exact 1-D minimiser z . (P_t - P_ee)
@@ -324,7 +325,7 @@ inline size_t poccd_smem(int nt) {   // the per-thread frames (24 B per joint) f
     return NMAX <= 18 ? (size_t)NMAX * nt * (sizeof(float4) + sizeof(float2)) : 0;
 }
 
-template <int NMAX, bool EXACT, bool REV>
+template <int NMAX, bool EXACT, int REV>
 static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                   const float* seeds, float* theta, float* cost, float* ep, float* eo,
                                   int32_t* iters, uint32_t* trace, uint32_t* ready, cudaStream_t s) {
@@ -382,9 +383,11 @@ template <int NMAX, bool EXACT>
 cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                            const float* seeds, float* theta, float* cost, float* ep, float* eo,
                            int32_t* iters, uint32_t* trace, uint32_t* ready, cudaStream_t s) {
+    if (rb.pmask == 0u && rb.rx)
+        return launch_poccd_r<NMAX, EXACT, 2>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
     if (rb.pmask == 0u)
-        return launch_poccd_r<NMAX, EXACT, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
-    return launch_poccd_r<NMAX, EXACT, false>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
+        return launch_poccd_r<NMAX, EXACT, 1>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
+    return launch_poccd_r<NMAX, EXACT, 0>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
 }
 
 }  // namespace hjcd

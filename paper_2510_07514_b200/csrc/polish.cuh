@@ -90,7 +90,7 @@ __device__ __forceinline__ T cost_w(const T (&W)[6], const T (&rho)[6]) {
     return T(0.5) * s;
 }
 
-template <int NMAX, bool EXACT = false, bool REV = false, class T>
+template <int NMAX, bool EXACT = false, int REV = 0, class T>
 __device__ __forceinline__ ResidT<T> eval_at(const DevRobotT<T>& rb, const TargetT<T>& tg, const T (&th)[NMAX]) {
     vec3<T> P[NMAX], Z[NMAX];   // unused (FRAMES = false), eliminated
     vec3<T> pe;
