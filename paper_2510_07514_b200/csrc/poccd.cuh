@@ -295,7 +295,43 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
                     if (j == ja) th[j] = clampf(th[j] + da, rb.j[j].lo, rb.j[j].hi);
                 }
             }
-        } else {
+        }
+        if constexpr (TEXIT && FRAMES_SMEM && NMAX > 8) {
+            // K12: the rejected seeds' Philox draws (R11), spread over the warp
+            // (for >= 3 draws per seed; at n <= 8 the per-lane form is as fast):
+            // item (r, blk) = block blk of the r-th rejecting lane, its 4 normals
+            // left in that lane's (now dead) frame slot blk; then each rejecting
+            // lane applies its own, exactly as perturb() would
+            const unsigned rej = __ballot_sync(0xffffffffu, active && !accept);
+            if (rej) {
+                const int nb = EXACT ? (NMAX + 3) / 4 : (n + 3) / 4;
+                const int lane = (int)(threadIdx.x & 31);
+                const int items = __popc(rej) * nb;
+                for (int it = lane; it < items; it += 32) {
+                    const int r = it / nb, blk = it - r * nb;
+                    const int ol = (int)__fns(rej, 0u, r + 1);
+                    float g[4];
+                    normals4<true>(draw(c, tid, (uint32_t)(m - lane + ol), P_PERTURB, (uint32_t)k, (uint32_t)blk), g);
+                    s_frames[blk * blockDim.x + (threadIdx.x - lane + ol)] = make_float4(g[0], g[1], g[2], g[3]);
+                }
+                __syncwarp();
+                if (active && !accept) {
+#pragma unroll
+                    for (int blk = 0; blk < (NMAX + 3) / 4; ++blk) {
+                        if (EXACT || 4 * blk < n) {
+                            const float4 g4 = s_frames[blk * blockDim.x + threadIdx.x];
+                            const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const int j = 4 * blk + e;
+                                if (j < NMAX && (EXACT || j < n))
+                                    th[j] = clampf(th[j] + c.sigma_ccd * g[e], rb.j[j].lo, rb.j[j].hi);
+                            }
+                        }
+                    }
+                }
+            }
+        } else if (!accept) {
             perturb<NMAX, EXACT, true>(rb, c, th, c.sigma_ccd, tid, (uint32_t)m, P_PERTURB, (uint32_t)k);   // R11 (K5)
         }
     }
