@@ -9,6 +9,7 @@
 #include <math_constants.h>
 
 #include "hjcd_internal.h"
+#include "pk2.cuh"
 
 namespace hjcd {
 
@@ -142,6 +143,66 @@ __device__ __forceinline__ void sincos_b(float x, float* s, float* c) {
 }
 __device__ __forceinline__ void sincos_b(double x, double* s, double* c) { sincos(x, s, c); }
 
+// K14: fk() for REV = 2 in fp32 with the rotation held as packed column pairs
+// (rows 0-1 of each column in one f2, row 2 scalar) and (tx, ty) packed, so
+// every column update a*col + b*col' is one FMUL2 + one FFMA2 for rows 0-1
+// plus the scalar row 2: 22 instead of 33 issue slots per joint.  Same
+// operations per element as the scalar form below; outputs unpacked for free.
+template <int NMAX, bool FRAMES, bool EXACT, bool FAST>
+__device__ __forceinline__ void fk_rx2(const DevRobotT<float>& rb, const float (&th)[NMAX], float3 (&P)[NMAX],
+                                       float3 (&Z)[NMAX], float3& pe, Quat& qe) {
+    f2 C0 = mk2(1.f, 0.f), C1 = mk2(0.f, 1.f), C2 = mk2(0.f, 0.f);   // R[0,3], R[1,4], R[2,5]
+    float r6 = 0.f, r7 = 0.f, r8 = 1.f;                              // R[6], R[7], R[8]
+    f2 t01 = mk2(0.f, 0.f);
+    float tz = 0.f;
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) {
+        if (EXACT || j < rb.n) {
+            const DevJointT<float>& J = rb.j[j];
+            t01 = add2(t01, fma2(C2, bc2(J.t[2]), fma2(C1, bc2(J.t[1]), mul2(C0, bc2(J.t[0])))));
+            tz += r6 * J.t[0] + r7 * J.t[1] + r8 * J.t[2];
+            // N = R F_j with F_j.R = Rx(alpha): column 0 unchanged
+            const f2 N1 = fma2(C2, bc2(J.R[7]), mul2(C1, bc2(J.R[4])));
+            const f2 N2 = fma2(C2, bc2(J.R[8]), mul2(C1, bc2(J.R[5])));
+            const float n7 = r7 * J.R[4] + r8 * J.R[7];
+            const float n8 = r7 * J.R[5] + r8 * J.R[8];
+            if (FRAMES) {
+                float x, y;
+                unpk2(t01, x, y);
+                P[j] = make_float3(x, y, tz);
+                unpk2(N2, x, y);
+                Z[j] = make_float3(x, y, n8);
+            }
+            float s, c;
+            if constexpr (FAST) __sincosf(th[j], &s, &c);
+            else sincos_b(th[j], &s, &c);
+            // R = N Rz(theta): col0 = c N0 + s N1, col1 = c N1 - s N0
+            const f2 C0n = fma2(bc2(s), N1, mul2(bc2(c), C0));
+            C1 = fma2(bc2(-s), C0, mul2(bc2(c), N1));
+            C0 = C0n;
+            C2 = N2;
+            const float r6n = c * r6 + s * n7;
+            r7 = c * n7 - s * r6;
+            r6 = r6n;
+            r8 = n8;
+        }
+    }
+    float e[2];
+    f2 te = fma2(C2, bc2(rb.eet[2]), fma2(C1, bc2(rb.eet[1]), mul2(C0, bc2(rb.eet[0]))));
+    te = add2(t01, te);
+    unpk2(te, e[0], e[1]);
+    const float tzz = tz + (r6 * rb.eet[0] + r7 * rb.eet[1] + r8 * rb.eet[2]);
+    float E[9];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+        const f2 col = fma2(C2, bc2(rb.eeR[6 + cc]), fma2(C1, bc2(rb.eeR[3 + cc]), mul2(C0, bc2(rb.eeR[cc]))));
+        unpk2(col, E[cc], E[3 + cc]);
+        E[6 + cc] = r6 * rb.eeR[cc] + r7 * rb.eeR[3 + cc] + r8 * rb.eeR[6 + cc];
+    }
+    pe = make_float3(e[0], e[1], tzz);
+    qe = quat_from_rot(E);
+}
+
 // Forward kinematics (Eq. 1) with frames (Eq. 7 inputs):
 // T = F_1 Rz(th_1) F_2 Rz(th_2) ... F_n Rz(th_n) EE  (prismatic: Tz).
 // FRAMES: P[j] = joint origin, Z[j] = joint axis (world), before joint motion
@@ -156,6 +217,12 @@ __device__ __forceinline__ void sincos_b(double x, double* s, double* c) { sinco
 template <int NMAX, bool FRAMES, bool EXACT = false, bool FAST = false, int REV = 0, class T>
 __device__ __forceinline__ void fk(const DevRobotT<T>& rb, const T (&th)[NMAX], vec3<T> (&P)[NMAX],
                                    vec3<T> (&Z)[NMAX], vec3<T>& pe, QuatT<T>& qe) {
+    if constexpr (REV == 2 && sizeof(T) == 4 && NMAX <= 8) {   // (more spills above 8 DoF)
+#ifndef HJCD_NO_K14
+        fk_rx2<NMAX, FRAMES, EXACT, FAST>(rb, th, P, Z, pe, qe);
+        return;
+#endif
+    }
     T R[9] = {T(1), T(0), T(0), T(0), T(1), T(0), T(0), T(0), T(1)};
     T tx = T(0), ty = T(0), tz = T(0);
 #pragma unroll
