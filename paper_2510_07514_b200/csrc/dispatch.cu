@@ -6,6 +6,13 @@
 
 namespace hjcd {
 
+int poccd_nmax(int n) {   // must match launch_poccd's choice below
+    switch (n) {
+        case 7: case 8: case 12: case 14: case 18: case 24: return n;
+        default: return n <= 8 ? 8 : (n <= 16 ? 16 : 32);
+    }
+}
+
 cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                          const float* seeds, float* theta, float* cost, float* ep, float* eo,
                          int32_t* iters, cudaStream_t s, uint32_t* trace, uint32_t* ready) {

@@ -279,7 +279,7 @@ cudaError_t solve_linked(const hjcd_robot* r, const DevCfg& d, const float* targ
     link.cost = cost1;
     link.theta = theta1;
     int nt, CL;
-    texit_shape(d.M, nt, CL);
+    texit_shape(d.M, poccd_nmax(r->dof), nt, CL);
     link.need = (uint32_t)CL;
     link.Mpad = 2;
     while (link.Mpad < d.M) link.Mpad <<= 1;

@@ -66,10 +66,14 @@ struct StageLink {
 };
 
 // seeds per CTA (nt) and CTAs per cluster (CL) of the PO-CCD lockstep launch:
-// 128-thread CTAs (32 for M < 128), up to 16 per cluster (non-portable size
-// above 8), so M <= 2048
-inline void texit_shape(int M, int& nt, int& CL) {
-    nt = M < 128 ? (M + 31) / 32 * 32 : 128;
+// 128-thread CTAs (32 for M < 128), 256 for the 12- and 14-joint kernels
+// (measured: C4 -7 %; no change at 7-8 joints; the 16/18-joint kernels need
+// 170 registers, i.e. 3 CTAs of 128), up to 16 CTAs per cluster (non-portable
+// size above 8).  nmax: the kernel's joint bound (poccd_nmax).
+constexpr int poccd_cta(int nmax) { return (nmax > 8 && nmax <= 14) ? 256 : 128; }
+inline void texit_shape(int M, int nmax, int& nt, int& CL) {
+    const int big = poccd_cta(nmax);
+    nt = M < 128 ? (M + 31) / 32 * 32 : (M < big ? 128 : big);
     CL = (M + nt - 1) / nt;
 }
 
@@ -103,6 +107,9 @@ template <class T, int NMAX, bool EXACT>
 cudaError_t launch_coop_t(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
                           const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
                           cudaStream_t s, const StageLink& link);
+
+// the joint bound NMAX of the PO-CCD kernel launch_poccd picks for n DoF (dispatch.cu)
+int poccd_nmax(int n);
 
 // launchers (dispatch.cu, select.cu); all asynchronous on `s`
 cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, float* jac,

@@ -36,7 +36,7 @@ template <int NMAX>
 constexpr int poccd_min_blocks() { return NMAX <= 14 ? 4 : (NMAX <= 18 ? 3 : 2); }
 
 template <int NMAX, bool EXACT, bool TEXIT, int REV>
-__global__ void __launch_bounds__(128, poccd_min_blocks<NMAX>())
+__global__ void __launch_bounds__(poccd_cta(NMAX), poccd_min_blocks<NMAX>() * 128 / poccd_cta(NMAX))
 k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float* __restrict__ targets, int T, const float* __restrict__ seeds,
         float* __restrict__ theta_out, float* __restrict__ cost_out, float* __restrict__ ep_out,
@@ -366,12 +366,12 @@ static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const flo
                                   const float* seeds, float* theta, float* cost, float* ep, float* eo,
                                   int32_t* iters, uint32_t* trace, uint32_t* ready, cudaStream_t s) {
     static bool smem_attr = false;   // NMAX = 16: the frames copy is 48 KB, above the default limit
-    if (!smem_attr && poccd_smem<NMAX>(128) > 0) {
+    if (!smem_attr && poccd_smem<NMAX>(poccd_cta(NMAX)) > 0) {
         cudaError_t e;
         if ((e = cudaFuncSetAttribute(k_poccd<NMAX, EXACT, false, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)poccd_smem<NMAX>(128))) != cudaSuccess ||
+                                      (int)poccd_smem<NMAX>(poccd_cta(NMAX)))) != cudaSuccess ||
             (e = cudaFuncSetAttribute(k_poccd<NMAX, EXACT, true, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)poccd_smem<NMAX>(128))) != cudaSuccess)
+                                      (int)poccd_smem<NMAX>(poccd_cta(NMAX)))) != cudaSuccess)
             return e;
         smem_attr = true;
     }
@@ -385,7 +385,7 @@ static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const flo
         return cudaGetLastError();
     }
     int nt, CL;
-    texit_shape(c.M, nt, CL);
+    texit_shape(c.M, NMAX, nt, CL);
     if (CL > 16) return cudaErrorInvalidConfiguration;
     if (CL > 8) {
         static bool np = false;
