@@ -4,6 +4,7 @@
 // every lane reads the same joint at the same time (uniform loop index), so
 // each access is a broadcast and FFMAs take the constants as direct operands.
 #pragma once
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -90,6 +91,21 @@ __device__ __forceinline__ unsigned long long* probe_base(uint32_t* ready, int T
     return (unsigned long long*)(ready + ((T + 63) & ~63));
 }
 #endif
+
+// Kernel attributes (shared-memory opt-in, non-portable cluster size) are
+// per device: `done` is one call site's bitmask of devices already set.
+// Setting an attribute twice is harmless, so a race only repeats the call.
+template <class Fn>
+inline cudaError_t once_per_device(std::atomic<unsigned long long>& done, Fn&& fn) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    if ((e = fn()) != cudaSuccess) return e;
+    done.fetch_or(bit, std::memory_order_acq_rel);
+    return cudaSuccess;
+}
 
 // Philox purposes (R30)
 enum : uint32_t { P_INIT = 1, P_PERTURB = 2, P_REPL = 3, P_PJPERT = 4 };

@@ -365,6 +365,9 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
 #endif
 }
 
+// dynamic shared memory limit of k_pjik_coop: 227 KB per CTA minus its static arrays
+constexpr size_t kPjikMaxDynSmem = (size_t)226 * 1024;
+
 template <class T, int NMAX, bool EXACT, int REV>
 static cudaError_t launch_coop_r(const DevRobotT<T>& rb, const DevCfg& c, const float* targets, int T_,
                                  const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
@@ -376,14 +379,18 @@ static cudaError_t launch_coop_r(const DevRobotT<T>& rb, const DevCfg& c, const 
         smem = std::max(smem, (size_t)link.Mpad * sizeof(unsigned long long) + (size_t)used * NMAX * sizeof(float));
     // opt in to what this launch needs (the fp64 records at NMAX = 32 exceed the
     // 227 KB per-CTA limit above 160 polish seeds: a clean configuration error)
-    if (smem > (size_t)227 * 1024) return cudaErrorInvalidConfiguration;
-    static size_t attr = 48 * 1024;
-    if (smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pjik_coop<T, NMAX, EXACT, REV>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = smem;
-    }
+    if (smem > kPjikMaxDynSmem) return cudaErrorInvalidConfiguration;
+    // once per device: opt in to the most any launch of this kernel may use
+    // (capped at the per-CTA limit)
+    static std::atomic<unsigned long long> attr{0};
+    cudaError_t e = once_per_device(attr, [] {
+        const size_t mx = std::min(kPjikMaxDynSmem,
+                                   std::max(coop_smem_bytes<T, NMAX>(256), (size_t)8192 * sizeof(unsigned long long) +
+                                                                               (size_t)256 * NMAX * sizeof(float)));
+        return cudaFuncSetAttribute(k_pjik_coop<T, NMAX, EXACT, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)mx);
+    });
+    if (e != cudaSuccess) return e;
     if (!link.ready) {
         k_pjik_coop<T, NMAX, EXACT, REV><<<T_, block, smem, s>>>(rb, c, targets, seeds, theta, ep, eo, counts, iters,
                                                                  link);

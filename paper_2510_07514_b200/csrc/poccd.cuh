@@ -365,15 +365,17 @@ template <int NMAX, bool EXACT, int REV>
 static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                   const float* seeds, float* theta, float* cost, float* ep, float* eo,
                                   int32_t* iters, uint32_t* trace, uint32_t* ready, cudaStream_t s) {
-    static bool smem_attr = false;   // NMAX = 16: the frames copy is 48 KB, above the default limit
-    if (!smem_attr && poccd_smem<NMAX>(poccd_cta(NMAX)) > 0) {
-        cudaError_t e;
-        if ((e = cudaFuncSetAttribute(k_poccd<NMAX, EXACT, false, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)poccd_smem<NMAX>(poccd_cta(NMAX)))) != cudaSuccess ||
-            (e = cudaFuncSetAttribute(k_poccd<NMAX, EXACT, true, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)poccd_smem<NMAX>(poccd_cta(NMAX)))) != cudaSuccess)
-            return e;
-        smem_attr = true;
+    static std::atomic<unsigned long long> smem_attr{0};   // the frames copy may exceed the 48 KB default
+    if (poccd_smem<NMAX>(poccd_cta(NMAX)) > 0) {
+        const cudaError_t e = once_per_device(smem_attr, [] {
+            const int b = (int)poccd_smem<NMAX>(poccd_cta(NMAX));
+            cudaError_t e2 = cudaFuncSetAttribute(k_poccd<NMAX, EXACT, false, REV>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+            if (e2 == cudaSuccess)
+                e2 = cudaFuncSetAttribute(k_poccd<NMAX, EXACT, true, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+            return e2;
+        });
+        if (e != cudaSuccess) return e;
     }
     if (!c.ccd_early_exit) {
         const long long total = (long long)T * c.M;
@@ -388,13 +390,11 @@ static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const flo
     texit_shape(c.M, NMAX, nt, CL);
     if (CL > 16) return cudaErrorInvalidConfiguration;
     if (CL > 8) {
-        static bool np = false;
-        if (!np) {
-            cudaError_t e = cudaFuncSetAttribute(k_poccd<NMAX, EXACT, true, REV>,
-                                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            if (e != cudaSuccess) return e;
-            np = true;
-        }
+        static std::atomic<unsigned long long> np{0};
+        const cudaError_t e = once_per_device(np, [] {
+            return cudaFuncSetAttribute(k_poccd<NMAX, EXACT, true, REV>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        });
+        if (e != cudaSuccess) return e;
     }
     const long long grid = (long long)T * CL;
     if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;

@@ -130,13 +130,12 @@ cudaError_t launch_select_replicate(const DevRobot& rb, const DevCfg& c, const f
     int Mpad = 2;
     while (Mpad < c.M) Mpad <<= 1;
     const size_t smem = (size_t)Mpad * sizeof(unsigned long long);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_select_replicate, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             8192 * (int)sizeof(unsigned long long));
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static std::atomic<unsigned long long> attr_set{0};
+    cudaError_t e = once_per_device(attr_set, [] {
+        return cudaFuncSetAttribute(k_select_replicate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    8192 * (int)sizeof(unsigned long long));
+    });
+    if (e != cudaSuccess) return e;
     const int block = Mpad >= 1024 ? 512 : (Mpad >= 256 ? 256 : 128);
     k_select_replicate<<<T, block, smem, s>>>(rb, c, cost, theta, Mpad, seeds, kept);
     return cudaGetLastError();
