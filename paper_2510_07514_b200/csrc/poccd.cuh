@@ -32,6 +32,9 @@ namespace hjcd {
 // REV: every DoF joint is revolute (no per-joint type branches).
 // Occupancy target: 4 CTAs of 128 (<= 128 registers) up to 14 joints; the
 // 16- and 32-joint bounds would spill 1-1.6 KB at 128, so they get 170 / 255.
+#ifndef HJCD_FRAMES_SMEM_MAX
+#define HJCD_FRAMES_SMEM_MAX 32   // every bound: 24 B per joint and thread (98 KB per 128-thread CTA at 32)
+#endif
 template <int NMAX>
 constexpr int poccd_min_blocks() { return NMAX <= 14 ? 4 : (NMAX <= 18 ? 3 : 2); }
 
@@ -49,7 +52,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     __shared__ int s_flag[3];
     // the frames (P_j, z_j) of this iteration, per thread, so the two moved
     // joints' frames are two indexed loads instead of 2 x NMAX predicated selects
-    constexpr bool FRAMES_SMEM = NMAX <= 18;
+    constexpr bool FRAMES_SMEM = NMAX <= HJCD_FRAMES_SMEM_MAX;
     extern __shared__ float4 s_frames[];   // [NMAX][blockDim] (P.xyz, z.x), then float2 [NMAX][blockDim] (z.yz)
     if (TEXIT) {
         t = (int)(blockIdx.x / (unsigned)CL);
@@ -357,8 +360,8 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
 }
 
 template <int NMAX>
-inline size_t poccd_smem(int nt) {   // the per-thread frames (24 B per joint) for NMAX <= 18
-    return NMAX <= 18 ? (size_t)NMAX * nt * (sizeof(float4) + sizeof(float2)) : 0;
+inline size_t poccd_smem(int nt) {   // the per-thread frames (24 B per joint)
+    return NMAX <= HJCD_FRAMES_SMEM_MAX ? (size_t)NMAX * nt * (sizeof(float4) + sizeof(float2)) : 0;
 }
 
 template <int NMAX, bool EXACT, int REV>
