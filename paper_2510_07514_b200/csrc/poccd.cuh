@@ -154,7 +154,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         // are shared by all joints and the last term is -2 C S w |v.z|.
         float Cd, Sd;
         __sincosf(0.5f * dphi, &Sd, &Cd);
-        const float sv2 = sv * sv, wsv2 = qr.w * qr.w + sv2;
+        const float sv2 = sv * sv, w2 = qr.w * qr.w, wsv2 = w2 + sv2, ka = sv2 + wsv2;
         const float ob0 = Cd * Cd * sv2 + Sd * Sd * wsv2;
         const float ob1 = Sd * Sd, ob2 = 2.f * Cd * Sd * qr.w;
 
@@ -190,8 +190,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
                     sp = dot3(r2, r2);
                     // Eq. 11 (R5): delta(k) sgn(a . z_j) phi, sgn(0) = 0
                     const float vz = dot3(vq, z);
-                    const float sg = vz > 0.f ? 1.f : (vz < 0.f ? -1.f : 0.f);
-                    const float tsum = th[j] + sg * dphi;
+                    const float tsum = th[j] + (vz != 0.f ? copysignf(dphi, vz) : 0.f);
                     dor = clampf(tsum, J.lo, J.hi) - th[j];
                     // score (K2): |v'|^2 of q_err (x) q(z, -d), monotone in |omega'|
                     if (dor == 0.f) {
@@ -199,9 +198,12 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
                     } else if (tsum >= J.lo && tsum <= J.hi) {
                         const float avz = fabsf(vz);
                         so = ob0 - avz * fmaf(ob1, avz, ob2);   // K2b closed form
-                    } else {                              // clamped step: the same closed form at
-                        __sincosf(0.5f * dor, &s2, &c2);  // the effective d (C, S of d / 2, signed)
-                        so = c2 * c2 * sv2 + s2 * s2 * (wsv2 - vz * vz) - 2.f * c2 * s2 * qr.w * vz;
+                    } else {   // clamped step: the same closed form at the effective d, in
+                        // double angles: C^2 = (1 + cos d) / 2, S^2 = (1 - cos d) / 2, 2 C S = sin d
+                        float sd, cd;
+                        __sincosf(dor, &sd, &cd);
+                        const float vz2 = vz * vz;
+                        so = 0.5f * fmaf(cd, vz2 - w2, ka - vz2) - sd * (qr.w * vz);
                     }
                 } else {
                     // prismatic (R32): exact 1-D minimiser z . (P_t - P_ee)
