@@ -143,15 +143,22 @@ hjcd_status hjcd_workspace_size_host(const hjcd_robot* r, int32_t T, const hjcd_
  *   pos_err  device [T]        |P_t - P_ee(theta*)| metres
  *   ori_err  device [T]        |omega(theta*)| radians (Eq. 5)
  *   status   device [T]        HJCD_TARGET_*
- *   workspace device, >= hjcd_workspace_size bytes, 256-byte aligned. */
+ *   workspace device, >= hjcd_workspace_size bytes, 256-byte aligned; one
+ *            solve at a time per workspace (it holds the stage-1 seeds and,
+ *            with the per-target PO-CCD stop rule, per-target readiness counts).
+ * Asynchronous on `stream`: a memset of the readiness counts, the PO-CCD
+ * kernel, PJ-IK as its programmatic dependent launch (it starts on each target
+ * as soon as that target's stage 1 is in memory, K10) and the best
+ * select.  Results are bitwise those of hjcd_solve_timed's staged sequence. */
 hjcd_status hjcd_solve(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
                        float* q_out, float* pos_err, float* ori_err, int32_t* status,
                        void* workspace, size_t workspace_bytes, hjcd_stream_t stream);
 
 /* hjcd_solve that also records stage boundaries for live per-kernel timing:
- * events = NULL or an array of 5 caller-created CUDA events (cudaEvent_t,
- * created with timing enabled), recorded on `stream` before PO-CCD, after
- * PO-CCD, after top-K/replicate, after PJ-IK and after best-select. */
+ * events = NULL (then exactly hjcd_solve) or an array of 5 caller-created
+ * CUDA events (cudaEvent_t, created with timing enabled), recorded on `stream`
+ * before PO-CCD, after PO-CCD, after top-K/replicate, after PJ-IK and after
+ * best-select; with events the stages run as separate, serialised kernels. */
 hjcd_status hjcd_solve_timed(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
                              float* q_out, float* pos_err, float* ori_err, int32_t* status,
                              void* workspace, size_t workspace_bytes, hjcd_stream_t stream,
