@@ -630,3 +630,49 @@ def test_solve_f64_high_dof(hjcd_lib, cuda):
     assert np.abs(pe64 - N(pe)).max() < 1e-10 and success(pe64, oe64).all()
     with pytest.raises(hjcd_lib.HjcdError):
         hjcd_lib.solve_f64(rb, T(tg, cuda), hjcd_lib.config_from_params(params(M=256, K=16, B=192)))
+
+
+def test_concurrent_solves_on_two_streams(hjcd_lib, cuda):
+    """Two hjcd_solve calls in flight at once on two streams (distinct
+    workspaces, the K10 dependent launch on each) give the bytes of the same
+    calls run one after the other; so does a CUDA-graph replay of one."""
+    import torch
+    ch = inputs.panda()
+    rb = hjcd_lib.Robot(ch)
+    tg_a, _ = targets_for(ch, 300, start=11)
+    tg_b, _ = targets_for(ch, 200, start=5000)
+    cfg_a = hjcd_lib.config_from_params(params())
+    cfg_b = hjcd_lib.config_from_params(params(target_index_offset=5000))
+    ta, tb = T(tg_a, cuda), T(tg_b, cuda)
+    ref_a = hjcd_lib.solve(rb, ta, cfg_a)
+    ref_b = hjcd_lib.solve(rb, tb, cfg_b)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    wa, wb = hjcd_lib.Workspace(), hjcd_lib.Workspace()
+    for _ in range(3):
+        s1.wait_stream(torch.cuda.current_stream())
+        s2.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s1):
+            out_a = hjcd_lib.solve(rb, ta, cfg_a, workspace=wa, stream=s1)
+        with torch.cuda.stream(s2):
+            out_b = hjcd_lib.solve(rb, tb, cfg_b, workspace=wb, stream=s2)
+        torch.cuda.synchronize()
+        assert all(torch.equal(x, y) for x, y in zip(out_a, ref_a))
+        assert all(torch.equal(x, y) for x, y in zip(out_b, ref_b))
+    # graph capture of the dependent-launch sequence, replayed twice
+    wg = hjcd_lib.Workspace()
+    outs = [torch.empty_like(x) for x in ref_a]
+    sg = torch.cuda.Stream()
+    sg.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(sg):
+        hjcd_lib.solve(rb, ta, cfg_a, out=outs, workspace=wg, stream=sg)   # warm: workspace sized
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=sg):
+        hjcd_lib.solve(rb, ta, cfg_a, out=outs, workspace=wg, stream=sg)
+    for _ in range(2):
+        for x in outs:
+            x.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert all(torch.equal(x, y) for x, y in zip(outs, ref_a))
