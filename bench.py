@@ -399,6 +399,39 @@ def main():
                               "success": float((r[3] <= 1).float().mean()),
                               "fine_converged": float((r[3] == 0).float().mean())})
 
+    # ---------------- PAPER Table I protocol (SURVEY 8(d) P-proto, E1; context
+    # only): ONE target per solve, 100 Halton targets, M in {1..2000} seeds,
+    # K = min(50, M) and B = min(100, M) (SURVEY's reading) or B = 100 (the
+    # paper also calls M the "batch size"); mean device time per
+    # target and mean reported errors of the answers
+    paper_protocol = []
+    if not args.no_sweep and world == 1:
+        for rn in ("panda", "fetch_like8"):
+            ch = inputs.robot(rn)
+            rbp = hjcd.Robot(ch)
+            ths = torch.from_numpy(inputs.halton_configs(ch, 100).astype(np.float32)).to(dev)
+            tgs = hjcd.fk(rbp, ths).contiguous()
+            for Mp, Bp in ((1, 1), (1, 100), (10, 10), (10, 100), (100, 100), (1000, 100), (2000, 100)):
+                cp = hjcd.default_config(M=Mp, K=min(50, Mp), B=Bp)
+                sws = hjcd.Workspace()
+                hjcd.solve(rbp, tgs[:1].contiguous(), cp, workspace=sws)
+                lat, pes, oes, oks = [], [], [], []
+                for i in range(100):
+                    ci = hjcd.default_config(M=Mp, K=min(50, Mp), B=Bp, target_index_offset=i)
+                    ti = tgs[i:i + 1]
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    r = hjcd.solve(rbp, ti, ci, workspace=sws)
+                    b.record(stream)
+                    b.synchronize()
+                    lat.append(a.elapsed_time(b))
+                    pes.append(float(r[1][0]))
+                    oes.append(float(r[2][0]))
+                    oks.append(int(r[3][0]) <= 1)
+                paper_protocol.append({"robot": rn, "M": Mp, "K": min(50, Mp), "B": Bp, "targets": 100, "mean_ms_per_target": statistics.mean(lat),
+                                       "mean_pos_err_m": statistics.mean(pes), "mean_ori_err_rad": statistics.mean(oes),
+                                       "success": statistics.mean(oks)})
+
     # ---------------- end to end through the C ABI with host buffers
     tg_host = targets.cpu().pin_memory()
     outh = (torch.empty((Tg, n), dtype=torch.float32).pin_memory(), torch.empty(Tg).pin_memory(),
@@ -439,7 +472,7 @@ def main():
                "latency_note": "p50/p99 of the per-step batch latency (one hjcd_solve of all targets)",
                "success_rate_1mm_1deg": succ,
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "latency_vs_batch": sweep,
-               "dof_sweep": dof_sweep,
+               "dof_sweep": dof_sweep, "paper_protocol_table1": paper_protocol,
                "gpu_launches": 3 * args.steps,
                "gpu_launches_note": "per hjcd_solve step: k_poccd, k_pjik_coop (dependent launch), k_select_best "
                                     "(+ one memset of the per-target readiness counts)",
