@@ -296,8 +296,9 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
             for (int j = 0; j < NMAX; ++j) {
                 if (EXACT || j < n) {
                     // theta + d_eff, re-clamped so rounding never leaves [lo, hi]
-                    if (j == jb) th[j] = clampf(th[j] + db, rb.j[j].lo, rb.j[j].hi);
-                    if (j == ja) th[j] = clampf(th[j] + da, rb.j[j].lo, rb.j[j].hi);
+                    // (the other joints get + 0 and a no-op clamp: one select chain)
+                    const float d = j == jb ? db : (j == ja ? da : 0.f);
+                    th[j] = clampf(th[j] + d, rb.j[j].lo, rb.j[j].hi);
                 }
             }
         }
