@@ -456,24 +456,29 @@ __device__ __forceinline__ void sort_stage1_keys(const float* cost_t, int M, int
     }
 }
 
-// Alg. 2 l.7-8 (R15): joints j0..j0+3 of polish seed b < floor(B/K) K of
-// target t: kept seed b mod K, copy b / K; copies > 0 (or every copy with
-// repl_noise_all) get N(0, sigma_rep^2) from Philox (tid, b, REPL, 0, j / 4),
-// clamped to the fp32 limits.  theta1 is stage 1's [T][n][M], read through L2.
+// Alg. 2 l.7-8 (R15): joints 4 blk .. 4 blk + 3 (< n) of polish seed
+// b < floor(B/K) K of target t: kept seed b mod K, copy b / K; copies > 0 (or
+// every copy with repl_noise_all) get N(0, sigma_rep^2) from ONE Philox block
+// (tid, b, REPL, 0, blk), clamped to the fp32 limits.  theta1 is stage 1's
+// [T][n][M], read through L2.
 template <class R>
-__device__ __forceinline__ float replica_value(const R& rb, const DevCfg& c, const float* theta1,
-                                               const unsigned long long* keys, int t, int b, int j,
-                                               uint32_t tid) {
-    const int K = c.K, M = c.M;
+__device__ __forceinline__ void replica_block(const R& rb, const DevCfg& c, const float* theta1,
+                                              const unsigned long long* keys, int t, int b, int blk,
+                                              uint32_t tid, float v[4]) {
+    const int K = c.K, M = c.M, n = rb.n;
     const int rank = b % K, cp = b / K;
     const int src = (int)(keys[rank] & 0xffffffffu);
-    float v = __ldcg(theta1 + ((long long)t * rb.n + j) * M + src);
-    if (cp > 0 || c.repl_noise_all) {
-        float g[4];
-        normals4(draw(c, tid, (uint32_t)b, P_REPL, 0u, (uint32_t)(j >> 2)), g);
-        v = clampf(__fmaf_rn(c.sigma_rep, g[j & 3], v), (float)rb.j[j].lo, (float)rb.j[j].hi);
+    float g[4] = {0.f, 0.f, 0.f, 0.f};
+    const bool noisy = cp > 0 || c.repl_noise_all;
+    if (noisy) normals4(draw(c, tid, (uint32_t)b, P_REPL, 0u, (uint32_t)blk), g);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int j = 4 * blk + e;
+        if (j < n) {
+            v[e] = __ldcg(theta1 + ((long long)t * n + j) * M + src);
+            if (noisy) v[e] = clampf(__fmaf_rn(c.sigma_rep, g[e], v[e]), (float)rb.j[j].lo, (float)rb.j[j].hi);
+        }
     }
-    return v;
 }
 
 }  // namespace hjcd

@@ -110,10 +110,15 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
 #endif
         sort_stage1_keys(link.cost + (long long)t * c.M, c.M, link.Mpad, coop_raw);
         float* stage = (float*)(coop_raw + link.Mpad);   // [used][NMAX]
+        const int nb = (n + 3) / 4;   // one Philox block per 4 joints
 #pragma unroll 1
-        for (int e = b; e < used * n; e += nt) {
-            const int bb = e / n, j = e - bb * n;
-            stage[bb * NMAX + j] = replica_value(rb, c, link.theta, coop_raw, t, bb, j, tid);
+        for (int e = b; e < used * nb; e += nt) {
+            const int bb = e / nb, blk = e - bb * nb;
+            float v[4];
+            replica_block(rb, c, link.theta, coop_raw, t, bb, blk, tid, v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (4 * blk + q < n) stage[bb * NMAX + 4 * blk + q] = v[q];
         }
         __syncthreads();
 #pragma unroll

@@ -24,9 +24,12 @@ k_select_replicate(const __grid_constant__ DevRobot rb, const __grid_constant__ 
         for (int r = threadIdx.x; r < K; r += blockDim.x) kept[(long long)t * K + r] = (int32_t)(keys[r] & 0xffffffffu);
     const uint32_t tid = (uint32_t)(c.tid_offset + t);
     const int used = c.copies * K;
-    for (int e = threadIdx.x; e < B * n; e += blockDim.x) {
-        const int b = e / n, j = e - b * n;
-        seeds[((long long)t * B + b) * n + j] = b < used ? replica_value(rb, c, theta, keys, t, b, j, tid) : CUDART_NAN_F;
+    const int nb = (n + 3) / 4;   // one Philox block per 4 joints
+    for (int e = threadIdx.x; e < B * nb; e += blockDim.x) {
+        const int b = e / nb, blk = e - b * nb;
+        float v[4] = {CUDART_NAN_F, CUDART_NAN_F, CUDART_NAN_F, CUDART_NAN_F};
+        if (b < used) replica_block(rb, c, theta, keys, t, b, blk, tid, v);
+        for (int q = 0; q < 4 && 4 * blk + q < n; ++q) seeds[((long long)t * B + b) * n + 4 * blk + q] = v[q];
     }
 }
 
