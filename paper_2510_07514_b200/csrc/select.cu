@@ -8,6 +8,8 @@
 //     converged seeds first, then cost, then slot) with a warp-shuffle +
 //     shared-memory reduction of 64-bit keys (tier | cost bits | slot).
 //   k_fk: batched FK + Jacobian (Eqs. 1, 7), one thread per configuration.
+#include <type_traits>
+
 #include "kin.cuh"
 
 namespace hjcd {
@@ -96,7 +98,9 @@ k_select_best(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCf
     }
 }
 
-template <int NMAX>
+// REV: the chain specialisation of the stage kernels (kin.cuh fk), so this entry
+// point evaluates the same FK code path the solve does (K11 / K14)
+template <int NMAX, int REV>
 __global__ void __launch_bounds__(128)
 k_fk(const __grid_constant__ DevRobot rb, const float* __restrict__ q, int N, float* __restrict__ pose7,
      float* __restrict__ jac) {
@@ -108,7 +112,7 @@ k_fk(const __grid_constant__ DevRobot rb, const float* __restrict__ q, int N, fl
     for (int j = 0; j < NMAX; ++j) th[j] = (j < n) ? q[(long long)s * n + j] : 0.f;
     float3 P[NMAX], Z[NMAX], pe;
     Quat qe;
-    fk<NMAX, true>(rb, th, P, Z, pe, qe);
+    fk<NMAX, true, false, false, REV>(rb, th, P, Z, pe, qe);
     float* o = pose7 + 7ll * s;
     o[0] = pe.x; o[1] = pe.y; o[2] = pe.z;
     o[3] = qe.w; o[4] = qe.x; o[5] = qe.y; o[6] = qe.z;
@@ -161,9 +165,16 @@ template cudaError_t launch_select_best<double>(const DevRobot&, const DevCfg&, 
 cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, float* jac, cudaStream_t s) {
     const int block = 128;
     const int grid = (N + block - 1) / block;
-    if (rb.n <= 8) k_fk<8><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
-    else if (rb.n <= 16) k_fk<16><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
-    else k_fk<32><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+    const int kind = rb.pmask ? 0 : (rb.rx ? 2 : 1);
+    auto go = [&](auto nmax) {
+        constexpr int NM = decltype(nmax)::value;
+        if (kind == 2) k_fk<NM, 2><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+        else if (kind == 1) k_fk<NM, 1><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+        else k_fk<NM, 0><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+    };
+    if (rb.n <= 8) go(std::integral_constant<int, 8>());
+    else if (rb.n <= 16) go(std::integral_constant<int, 16>());
+    else go(std::integral_constant<int, 32>());
     return cudaGetLastError();
 }
 
