@@ -145,7 +145,9 @@ hjcd_status hjcd_workspace_size_host(const hjcd_robot* r, int32_t T, const hjcd_
  *   status   device [T]        HJCD_TARGET_*
  *   workspace device, >= hjcd_workspace_size bytes, 256-byte aligned; one
  *            solve at a time per workspace (it holds the stage-1 seeds and,
- *            with the per-target PO-CCD stop rule, per-target readiness counts).
+ *            with the per-target PO-CCD stop rule, per-target readiness counts;
+ *            a polish CTA that waits ~30 s for its target traps, so misuse
+ *            surfaces as HJCD_E_CUDA on a later call rather than a hang).
  * Asynchronous on `stream`: a memset of the readiness counts, the PO-CCD
  * kernel, PJ-IK as its programmatic dependent launch (it starts on each target
  * as soon as that target's stage 1 is in memory, K10) and the best

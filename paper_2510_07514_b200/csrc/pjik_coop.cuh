@@ -98,9 +98,12 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
         if (b == 0) {
             const uint32_t* f = link.ready + t;
             uint32_t v;
-            for (;;) {
+            for (uint32_t spins = 0;; ++spins) {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
                 if (v >= link.need) break;
+                // a stage 1 that cannot complete (e.g. one workspace shared by
+                // two solves in flight) becomes a CUDA error, not a hang (~30 s)
+                if (spins > (1u << 26)) __trap();
                 __nanosleep(500);
             }
         }
