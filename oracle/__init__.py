@@ -79,7 +79,8 @@ def lib():
         _lib.oracle_ccd.argtypes = [P, P, P, i32, i64, P, P, P, P]
         _lib.oracle_po_ccd_replay.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P, P]
         _lib.oracle_select_replicate.argtypes = [P, P, P, P, i32, i64, P, P]
-        _lib.oracle_pj_ik.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P]
+        _lib.oracle_pj_ik.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P, P]
+        _lib.oracle_pj_ik_replay.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P, P, P, P]
         _lib.oracle_solve.argtypes = [P, P, P, i32, i64, P, P, P, P]
         _lib.oracle_line_search.argtypes = [P, P, P, P, P]
         _lib.oracle_lm_step.argtypes = [P, P, i32, P, P, P]
@@ -308,9 +309,10 @@ def select_replicate(chain, params, cost, theta, tid_offset: int = 0):
     return seeds, kept
 
 
-def pj_ik(chain, params, targets, seeds, tid_offset: int = 0):
+def pj_ik(chain, params, targets, seeds, tid_offset: int = 0, trace: bool = False):
     """Alg. 4: seeds [T,B,n] -> dict theta [T,B,n], ep, eo, margin, iters [T,B],
-    counts [T,B,4]."""
+    counts [T,B,4] (+ trace [T,B,lm_iters]: its own decision words, pj_word
+    format; 0 where no step was taken)."""
     r, c = make_robot(chain), make_config(params)
     tg = np.ascontiguousarray(targets, dtype=np.float32).reshape(-1, 7)
     sd = np.ascontiguousarray(seeds, dtype=np.float64)
@@ -319,9 +321,44 @@ def pj_ik(chain, params, targets, seeds, tid_offset: int = 0):
     out = dict(theta=np.empty((T, B, n)), ep=np.empty((T, B)), eo=np.empty((T, B)),
                counts=np.empty((T, B, 4), dtype=np.int32), margin=np.empty((T, B)),
                iters=np.empty((T, B), dtype=np.int32))
+    if trace:
+        out["trace"] = np.zeros((T, B, max(params["lm_iters"], 1)), dtype=np.uint32)
     lib().oracle_pj_ik(_ref(r), _ref(c), _p(tg), T, tid_offset, _p(sd), _p(out["theta"]),
                        _p(out["ep"]), _p(out["eo"]), _p(out["counts"]), _p(out["margin"]),
-                       _p(out["iters"]))
+                       _p(out["iters"]), _p(out.get("trace")))
+    return out
+
+
+# decision word of PJ-IK (hjcd_pjik_trace / the oracle's own trace)
+PJ_LM, PJ_DOGLEG, PJ_SINGLE, PJ_PERTURB = 0, 1, 2, 3
+
+
+def pj_word_fields(w):
+    """(kind, alpha index, single-coordinate index, step-taken flag) of decision words."""
+    w = np.asarray(w, dtype=np.uint32)
+    return w & 3, (w >> 2) & 31, (w >> 8) & 31, (w >> 15) & 1
+
+
+def pj_ik_replay(chain, params, targets, seeds, trace, iters, tid_offset: int = 0):
+    """Alg. 4 in fp64 following recorded decisions (hjcd_pjik_trace words,
+    trace [T,B,lm_iters] uint32, iters [T,B]) -> dict theta [T,B,n], ep, eo,
+    counts [T,B,4], gap [T,B] (how much worse any recorded decision is than the
+    fp64 one, residual-norm units), stop_gap [T], gap_at [T,B] (8 k + kind:
+    1 LM trial, 2 dogleg, 3 single index, 4 single trial, 5 continued inside the
+    fine box, 6 invalid word; -1 none)."""
+    r, c = make_robot(chain), make_config(params)
+    tg = np.ascontiguousarray(targets, dtype=np.float32).reshape(-1, 7)
+    sd = np.ascontiguousarray(seeds, dtype=np.float64)
+    T, B, n = sd.shape
+    I = params["lm_iters"]
+    tr = np.ascontiguousarray(trace, dtype=np.uint32).reshape(T, B, I)
+    it = np.ascontiguousarray(iters, dtype=np.int32).reshape(T, B)
+    out = dict(theta=np.full((T, B, n), np.nan), ep=np.full((T, B), np.nan), eo=np.full((T, B), np.nan),
+               counts=np.zeros((T, B, 4), dtype=np.int32), gap=np.zeros((T, B)), stop_gap=np.empty(T),
+               gap_at=np.full((T, B), -1, dtype=np.int32))
+    lib().oracle_pj_ik_replay(_ref(r), _ref(c), _p(tg), T, tid_offset, _p(sd), _p(tr), _p(it), _p(out["theta"]),
+                              _p(out["ep"]), _p(out["eo"]), _p(out["counts"]), _p(out["gap"]),
+                              _p(out["stop_gap"]), _p(out["gap_at"]))
     return out
 
 

@@ -919,10 +919,18 @@ bool pj_ik_check(const Robot& rb, const OracleConfig& c, const Target& tgt,
     return cp && co;
 }
 
+/* PJ-IK decision word (the format of hjcd_pjik_trace, include/hjcd.h): the
+ * branch that moved the seed (0 LM step, 1 dogleg, 2 single coordinate,
+ * 3 perturbation) | alpha index a (step beta^-a) << 2 | single-coordinate
+ * index i* << 8 | 1 << 15 (a step was taken; 0 = no step at this iteration) */
+uint32_t pj_word(int kind, int a, int ist) {
+    return (uint32_t)kind | ((uint32_t)a << 2) | ((uint32_t)ist << 8) | (1u << 15);
+}
+
 /* one iteration of Alg. 4 (l.3-17) for one seed, frames F and residual e at th */
 void pj_ik_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
                 uint32_t bidx, int k, const Frames& F, const Err& e, std::vector<double>& th,
-                PolishOut& po) {
+                PolishOut& po, uint32_t* record = nullptr) {
     const OracleRobot* r = rb.r;
     int n = rb.dof;
     Frames Ft;
@@ -937,7 +945,11 @@ void pj_ik_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint6
     if (ok) {
         for (int j = 0; j < n; ++j) dth[j] = clampd(dth[j], -c.R, c.R); /* l.6, R21 */
         int a = line_search(rb, c, tgt, th, dth.data(), W, c0, tt, &po.margin);
-        if (a >= 0) { th = tt; po.counts[0]++; return; }
+        if (a >= 0) {
+            th = tt; po.counts[0]++;
+            if (record) *record = pj_word(0, a, 0);
+            return;
+        }
     }
     /* dogleg (l.10-12), acceptance on the unweighted |rho| (R23) */
     if (dogleg_step(c, J.data(), n, rho, dth.data())) {
@@ -948,7 +960,11 @@ void pj_ik_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint6
         rho_of(et, rt);
         double n0 = norm6(rho), nt = norm6(rt);
         po.margin = std::min(po.margin, rel_gap(nt, n0, 1e-30));
-        if (nt < n0) { th = tt; po.counts[1]++; return; }
+        if (nt < n0) {
+            th = tt; po.counts[1]++;
+            if (record) *record = pj_word(1, 0, 0);
+            return;
+        }
     }
     /* single coordinate (l.13-16) */
     double gap;
@@ -956,13 +972,140 @@ void pj_ik_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint6
     if (ist >= 0) {
         po.margin = std::min(po.margin, gap);
         int a = line_search(rb, c, tgt, th, dth.data(), W, c0, tt, &po.margin);
-        if (a >= 0) { th = tt; po.counts[2]++; return; }
+        if (a >= 0) {
+            th = tt; po.counts[2]++;
+            if (record) *record = pj_word(2, a, ist);
+            return;
+        }
     }
     /* perturbation (l.17, R25) */
     for (int j = 0; j < n; ++j) {
         int ent = rb.dof_entry[j];
         double g = normal_for_joint(c.rng_seed, tid, bidx, P_PJPERT, (uint32_t)k, j);
         th[j] = clampd(th[j] + c.sigma_lm * g, r->lo[ent], r->hi[ent]);
+    }
+    po.counts[3]++;
+    if (record) *record = pj_word(3, 0, 0);
+}
+
+/* Decision replay of one Alg. 4 iteration (oracle_pj_ik_replay): the same
+ * cascade as pj_ik_step, in fp64, but the branch, alpha index and
+ * single-coordinate index are the RECORDED ones (word, pj_word format).  Every
+ * cascade item before the recorded one must fail and the recorded one must
+ * succeed; *gap grows by how far the fp64 comparison is from the recorded
+ * outcome, in the units it compares: | |W rho_t| - |W rho_0| | for the
+ * weighted-cost tests (Eq. 13, R22), | |rho_t| - |rho_0| | for the dogleg test
+ * (R23), |g_i*| - |g_rec| for the single-coordinate argmax (Eq. 16, R24).
+ * gap_kind: 1 LM trial, 2 dogleg trial, 3 single-coordinate index, 4
+ * single-coordinate trial, 6 an invalid word. */
+void pj_ik_step_replay(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
+                       uint32_t bidx, int k, const Frames& F, const Err& e, std::vector<double>& th,
+                       PolishOut& po, uint32_t word, double* gap, int* gap_kind) {
+    const OracleRobot* r = rb.r;
+    int n = rb.dof;
+    auto upd = [&](double g, int kind) { if (g > *gap) { *gap = g; *gap_kind = kind; } };
+    int kind = (int)(word & 3u), af = (int)((word >> 2) & 31u), istf = (int)((word >> 8) & 31u);
+    if (!(word & (1u << 15)) || (word >> 16) != 0 || af > c.A || istf >= n ||
+        (kind == 1 && af != 0)) {
+        upd(INF, 6);
+        return;
+    }
+    Frames Ft;
+    std::vector<double> J(6 * n), dth(n), tt(n);
+    jacobian(rb, F, J.data());
+    double W[6], rho[6];
+    weights(c, J.data(), n, W);
+    rho_of(e, rho);
+    double c0 = cost_w(W, rho);
+    /* the weighted cost at clamp(th + alpha dth) (Eq. 13, W frozen at th) */
+    auto trial_cost = [&](const std::vector<double>& d, double alpha) {
+        trial_point(rb, th, d.data(), alpha, tt);
+        fk(rb, tt.data(), Ft);
+        Err et = residual(Ft, tgt);
+        double rt[6];
+        rho_of(et, rt);
+        return cost_w(W, rt);
+    };
+    auto depth = [&](double ct) { return std::fabs(std::sqrt(2.0 * ct) - std::sqrt(2.0 * c0)); };
+    /* LM line search (l.3-9): items alpha_0 .. alpha_A */
+    bool lm_ok = lm_step(c, J.data(), n, W, rho, dth.data());
+    if (lm_ok)
+        for (int j = 0; j < n; ++j) dth[j] = clampd(dth[j], -c.R, c.R);
+    double alpha = 1.0;
+    for (int a = 0; a <= c.A; ++a, alpha /= c.beta) {
+        bool forced_here = kind == 0 && a == af;
+        if (!lm_ok) {
+            if (forced_here) { upd(INF, 1); return; }
+            continue;
+        }
+        double ct = trial_cost(dth, alpha);
+        if (forced_here) {
+            if (!(ct < c0)) upd(depth(ct), 1);
+            th = tt; po.counts[0]++;
+            return;
+        }
+        if (ct < c0) upd(depth(ct), 1);   /* fp64 accepts an earlier item */
+    }
+    /* dogleg (l.10-12) */
+    std::vector<double> dd(n);
+    if (dogleg_step(c, J.data(), n, rho, dd.data())) {
+        trial_point(rb, th, dd.data(), 1.0, tt);
+        fk(rb, tt.data(), Ft);
+        Err et = residual(Ft, tgt);
+        double rt[6];
+        rho_of(et, rt);
+        double n0 = norm6(rho), nt = norm6(rt);
+        if (kind == 1) {
+            if (!(nt < n0)) upd(std::fabs(nt - n0), 2);
+            th = tt; po.counts[1]++;
+            return;
+        }
+        if (nt < n0) upd(std::fabs(nt - n0), 2);
+    } else if (kind == 1) {
+        upd(INF, 2);
+        return;
+    }
+    /* single coordinate (l.13-16) at the recorded index */
+    std::vector<double> g(n);
+    for (int a = 0; a < n; ++a) {
+        double s = 0;
+        for (int i = 0; i < 6; ++i) s += J[i * n + a] * W[i] * W[i] * rho[i];
+        g[a] = s;
+    }
+    int ist = 0;
+    for (int a = 1; a < n; ++a)
+        if (std::fabs(g[a]) > std::fabs(g[ist])) ist = a;
+    bool sc_ok = g[ist] != 0.0;
+    if (kind == 2) {
+        upd(std::fabs(g[ist]) - std::fabs(g[istf]), 3);
+        ist = istf;
+        sc_ok = g[ist] != 0.0;
+    }
+    std::vector<double> ds(n, 0.0);
+    if (sc_ok) {
+        double m = std::min(std::fabs(g[ist]), c.R);
+        ds[ist] = (g[ist] > 0) ? -m : m;
+    }
+    alpha = 1.0;
+    for (int a = 0; a <= c.A; ++a, alpha /= c.beta) {
+        bool forced_here = kind == 2 && a == af;
+        if (!sc_ok) {
+            if (forced_here) { upd(INF, 4); return; }
+            continue;
+        }
+        double ct = trial_cost(ds, alpha);
+        if (forced_here) {
+            if (!(ct < c0)) upd(depth(ct), 4);
+            th = tt; po.counts[2]++;
+            return;
+        }
+        if (ct < c0) upd(depth(ct), 4);
+    }
+    /* perturbation (l.17, R25): every item above failed */
+    for (int j = 0; j < n; ++j) {
+        int ent = rb.dof_entry[j];
+        double gn = normal_for_joint(c.rng_seed, tid, bidx, P_PJPERT, (uint32_t)k, j);
+        th[j] = clampd(th[j] + c.sigma_lm * gn, r->lo[ent], r->hi[ent]);
     }
     po.counts[3]++;
 }
@@ -978,7 +1121,7 @@ PolishOut polish_init() {
 
 /* Alg. 4 for ONE seed with a per-seed break (target_early_exit = 0) */
 PolishOut pj_ik_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
-                     uint32_t bidx, std::vector<double>& th) {
+                     uint32_t bidx, std::vector<double>& th, uint32_t* record = nullptr) {
     PolishOut po = polish_init();
     Frames F;
     Err e;
@@ -986,7 +1129,7 @@ PolishOut pj_ik_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, 
     for (k = 0;; ++k) {
         if (pj_ik_check(rb, c, tgt, th, F, e, po)) break;
         if (k == c.lm_iters) break;
-        pj_ik_step(rb, c, tgt, tid, bidx, k, F, e, th, po);
+        pj_ik_step(rb, c, tgt, tid, bidx, k, F, e, th, po, record ? record + k : nullptr);
     }
     po.iters = k;
     return po;
@@ -998,7 +1141,8 @@ PolishOut pj_ik_seed(const Robot& rb, const OracleConfig& c, const Target& tgt, 
  * test (Alg. 4 l.18 "break"), every seed keeping its state after
  * the same number of iterations (R26b).  th_bn: [used][n] in/out. */
 void pj_ik_target(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid, int used,
-                  std::vector<std::vector<double>>& th_bn, std::vector<PolishOut>& po) {
+                  std::vector<std::vector<double>>& th_bn, std::vector<PolishOut>& po,
+                  uint32_t* record = nullptr, int rec_stride_b = 0) {
     po.assign(used, polish_init());
     std::vector<Frames> F(used);
     std::vector<Err> e(used);
@@ -1011,7 +1155,8 @@ void pj_ik_target(const Robot& rb, const OracleConfig& c, const Target& tgt, uin
         for (int b = 0; b < used; ++b) po[b].iters = k;
         if (any || k == c.lm_iters) break;
         for (int b = 0; b < used; ++b)
-            pj_ik_step(rb, c, tgt, tid, (uint32_t)b, k, F[b], e[b], th_bn[b], po[b]);
+            pj_ik_step(rb, c, tgt, tid, (uint32_t)b, k, F[b], e[b], th_bn[b], po[b],
+                       record ? record + (size_t)b * rec_stride_b + k : nullptr);
     }
 }
 
@@ -1313,12 +1458,14 @@ void oracle_select_replicate(const OracleRobot* r, const OracleConfig* c, const 
 
 /* PJ-IK stage (Alg. 4): seeds f64 [T][B][n] -> theta f64 [T][B][n], ep/eo f64
  * [T][B], counts i32 [T][B][4] (LM, dogleg, single, perturb), margin f64 [T][B]
- * (smallest relative decision margin), iters i32 [T][B] */
+ * (smallest relative decision margin), iters i32 [T][B], trace u32
+ * [T][B][lm_iters] or NULL (this oracle's own decision words, pj_word format;
+ * 0 where no step was taken) */
 void oracle_pj_ik(const OracleRobot* r, const OracleConfig* c, const float* targets, int32_t T,
                   int64_t tid_offset, const double* seeds, double* theta, double* ep, double* eo,
-                  int32_t* counts, double* margin, int32_t* iters) {
+                  int32_t* counts, double* margin, int32_t* iters, uint32_t* trace) {
     Robot rb = make_robot(r);
-    int n = rb.dof, B = c->B;
+    int n = rb.dof, B = c->B, I = c->lm_iters;
     int used = (c->B / c->K) * c->K;
     auto emit = [&](size_t o, const std::vector<double>& th, const PolishOut& po) {
         for (int j = 0; j < n; ++j) theta[o * n + j] = th[j];
@@ -1338,7 +1485,8 @@ void oracle_pj_ik(const OracleRobot* r, const OracleConfig* c, const float* targ
                 th[b].assign(seeds + o * n, seeds + o * n + n);
             }
             std::vector<PolishOut> po;
-            pj_ik_target(rb, *c, tgt, (uint64_t)(tid_offset + t), used, th, po);
+            pj_ik_target(rb, *c, tgt, (uint64_t)(tid_offset + t), used, th, po,
+                         trace ? trace + (size_t)t * B * I : nullptr, I);
             for (int b = 0; b < used; ++b) emit((size_t)t * B + b, th[b], po[b]);
         }
         return;
@@ -1349,9 +1497,77 @@ void oracle_pj_ik(const OracleRobot* r, const OracleConfig* c, const float* targ
             Target tgt = read_target(targets + (size_t)t * 7);
             size_t o = (size_t)t * B + b;
             std::vector<double> th(seeds + o * n, seeds + o * n + n);
-            PolishOut po = pj_ik_seed(rb, *c, tgt, (uint64_t)(tid_offset + t), (uint32_t)b, th);
+            PolishOut po = pj_ik_seed(rb, *c, tgt, (uint64_t)(tid_offset + t), (uint32_t)b, th,
+                                      trace ? trace + o * I : nullptr);
             emit(o, th, po);
         }
+    }
+}
+
+/* Decision replay of Alg. 4 (parity tests, DESIGN.md §4 "decision replay"):
+ * every polish seed runs the GPU's iteration count iters [T][B] and, at each
+ * iteration k, takes the GPU's recorded decision trace [T][B][lm_iters]
+ * (hjcd_pjik_trace word = pj_word: branch | alpha index << 2 | i* << 8 |
+ * 1 << 15) in place of its own, with J, W, every direction, trial and
+ * perturbation computed here in fp64 as in pj_ik_step (pj_ik_step_replay).
+ *   gap [T][B]: the largest amount by which a recorded decision is worse than
+ *     this oracle's own (residual-norm units, see pj_ik_step_replay), and the
+ *     depth inside the fine box (min(eps_p - ep, eps_o - eo)) at an iteration
+ *     the GPU continued; 0 = all agree;
+ *   gap_at [T][B] (or NULL): 8 k + kind of that largest gap (kinds of
+ *     pj_ik_step_replay, 5 = continued inside the box), -1 none;
+ *   stop_gap [T]: the distance outside the fine box of the seed closest to it
+ *     where the GPU stopped before lm_iters (per target with
+ *     target_early_exit, else the max over the seeds of their own); 0 if none.
+ * theta f64 [T][B][n], ep/eo f64 [T][B], counts i32 [T][B][4] after the replay
+ * (slots >= floor(B/K) K untouched). */
+void oracle_pj_ik_replay(const OracleRobot* r, const OracleConfig* c, const float* targets, int32_t T,
+                         int64_t tid_offset, const double* seeds, const uint32_t* trace, const int32_t* iters,
+                         double* theta, double* ep, double* eo, int32_t* counts, double* gap,
+                         double* stop_gap, int32_t* gap_at) {
+    Robot rb = make_robot(r);
+    int n = rb.dof, B = c->B, I = c->lm_iters;
+    int used = (c->B / c->K) * c->K;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int t = 0; t < T; ++t) {
+        Target tgt = read_target(targets + (size_t)t * 7);
+        uint64_t tid = (uint64_t)(tid_offset + t);
+        double sg = c->target_early_exit ? INF : 0.0;
+        bool stopped = false;
+        for (int b = 0; b < used; ++b) {
+            size_t o = (size_t)t * B + b;
+            std::vector<double> th(seeds + o * n, seeds + o * n + n);
+            PolishOut po = polish_init();
+            Frames F;
+            Err e;
+            double g = 0.0;
+            int K = iters[o], kind = 0, at = -1;
+            for (int k = 0;; ++k) {
+                pj_ik_check(rb, *c, tgt, th, F, e, po);
+                double inside = std::min(c->eps_p_fine - e.ep, c->eps_o_fine - e.eo);
+                if (k == K) {
+                    if (K < I) {
+                        double outside = std::max(0.0, -inside);
+                        stopped = true;
+                        sg = c->target_early_exit ? std::min(sg, outside) : std::max(sg, outside);
+                    }
+                    break;
+                }
+                if (k >= I) { g = INF; at = 8 * k + 6; break; }   /* more iterations than the budget */
+                if (inside > g) { g = inside; at = 8 * k + 5; }
+                double g0 = g;
+                pj_ik_step_replay(rb, *c, tgt, tid, (uint32_t)b, k, F, e, th, po, trace[o * I + k], &g, &kind);
+                if (g > g0) at = 8 * k + kind;
+                if (!std::isfinite(g)) break;
+            }
+            for (int j = 0; j < n; ++j) theta[o * n + j] = th[j];
+            ep[o] = po.ep;
+            eo[o] = po.eo;
+            if (counts) for (int i = 0; i < 4; ++i) counts[o * 4 + i] = po.counts[i];
+            gap[o] = g;
+            if (gap_at) gap_at[o] = at;
+        }
+        stop_gap[t] = stopped ? sg : 0.0;
     }
 }
 
