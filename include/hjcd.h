@@ -49,7 +49,8 @@ typedef enum {
     HJCD_E_INVALID_ARG = 1, /* null pointer, bad size, K > M, K > B, lo > hi, ... */
     HJCD_E_UNSUPPORTED = 2, /* dof > HJCD_MAX_DOF, unsupported option */
     HJCD_E_CUDA = 3,        /* a CUDA runtime error (see hjcd_last_cuda_error) */
-    HJCD_E_WORKSPACE = 4,   /* workspace too small or misaligned (< 256 B alignment) */
+    HJCD_E_WORKSPACE = 4,   /* workspace too small, misaligned (< 256 B), or in use by a
+                               solve still in flight on another stream */
     HJCD_E_NOMEM = 5        /* host allocation failed */
 } hjcd_status;
 
@@ -145,9 +146,17 @@ hjcd_status hjcd_workspace_size_host(const hjcd_robot* r, int32_t T, const hjcd_
  *   status   device [T]        HJCD_TARGET_*
  *   workspace device, >= hjcd_workspace_size bytes, 256-byte aligned; one
  *            solve at a time per workspace (it holds the stage-1 seeds and,
- *            with the per-target PO-CCD stop rule, per-target readiness counts;
- *            a polish CTA that waits ~30 s for its target traps, so misuse
- *            surfaces as HJCD_E_CUDA on a later call rather than a hang).
+ *            with the per-target PO-CCD stop rule, per-target readiness
+ *            counts).  A solve on another stream while the last solve that
+ *            used this workspace (through this library, any solve entry point)
+ *            is still in flight returns HJCD_E_WORKSPACE; the same stream is
+ *            stream-ordered and always allowed; during CUDA-graph capture the
+ *            check is skipped.  If a polish CTA still waits more than ~30 s
+ *            (x ccd_iters/64) for its target's stage 1 (e.g. a workspace shared
+ *            with another process), it executes a device trap rather than
+ *            hang: that is a sticky error that loses the CUDA context of the
+ *            whole process (every later CUDA call in it, torch's included,
+ *            fails).
  * Asynchronous on `stream`: a memset of the readiness counts, the PO-CCD
  * kernel, PJ-IK as its programmatic dependent launch (it starts on each target
  * as soon as that target's stage 1 is in memory, K10) and the best
@@ -200,6 +209,22 @@ hjcd_status hjcd_solve_host(const hjcd_robot* r, const hjcd_config* c, const flo
 
 /* ---- stage entry points (tests, tracing; same conventions; device pointers) ---- */
 
+/* hjcd_fk with the joint sines / cosines from the SFU (__sincosf), the
+ * variant the PO-CCD kernel runs (K5: coarse stage only); same
+ * layouts and errors as hjcd_fk.  For parity testing of that FK. */
+hjcd_status hjcd_fk_sfu(const hjcd_robot* r, const float* q, int32_t N, float* pose7, float* jac,
+                        hjcd_stream_t stream);
+
+/* Pose error of given joint configurations, evaluated in fp64 on the fp64
+ * copy of the chain: pos_err = |P_t - P_ee(q)| (Eq. 4) and ori_err = |omega|
+ * (Eq. 5, R1) with the fp32 configuration widened exactly.  Lets a caller
+ * decide success at 1 mm / 1 deg from the returned theta rather than from the
+ * solver's own fp32 errors (SURVEY §8(d) "Success").
+ *   q [N][dof] f32, targets [N][7] f32 in (device); pos_err, ori_err [N] f64
+ *   out (device).  An invalid target row (S2) gives +inf.  Asynchronous. */
+hjcd_status hjcd_pose_error_f64(const hjcd_robot* r, const float* q, const float* targets, int32_t N,
+                                double* pos_err, double* ori_err, hjcd_stream_t stream);
+
 /* Batched FK (Eq. 1) + geometric Jacobian (Eq. 7) for N configurations.
  *   q     [N][dof]; pose7 [N][7] (w >= 0); jac [N][6][dof] or NULL
  *   (rows 0-2 linear, 3-5 angular; prismatic columns [z; 0]). */
@@ -223,10 +248,16 @@ hjcd_status hjcd_poccd(const hjcd_robot* r, const hjcd_config* c, const float* t
  *   bits 0-4 jp, 5-9 jo (Alg. 3 l.9 argmins), bit 10 same joint and the
  *   orientation step taken (l.10), bit 11 accepted (l.11), bits 12-13 / 14-15
  *   the sign of the position / orientation step at jp / jo (0 zero,
- *   1 positive, 2 negative). */
+ *   1 positive, 2 negative).
+ *   theta_hist [T][M][ccd_iters + 1][dof] out (device) or NULL: each seed's
+ *   theta at the start of every iteration it ran (entry k = the state the
+ *   decision of word k was taken at; entry iters = the returned theta); the
+ *   decision replay restarts the oracle from it at every iteration, so fp32
+ *   drift cannot accumulate into the comparison. */
 hjcd_status hjcd_poccd_trace(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
                              const float* seeds, float* theta, float* cost, float* pos_err,
-                             float* ori_err, int32_t* iters, uint32_t* trace, hjcd_stream_t stream);
+                             float* ori_err, int32_t* iters, uint32_t* trace, float* theta_hist,
+                             hjcd_stream_t stream);
 
 /* Classic position-only CCD (Alg. 1), the baseline PO-CCD extends
  * (ablation): T targets x c->M seeds, joints swept tip to root,
@@ -254,6 +285,26 @@ hjcd_status hjcd_select_replicate(const hjcd_robot* r, const hjcd_config* c, con
 hjcd_status hjcd_pjik(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
                       const float* seeds, float* theta, float* pos_err, float* ori_err,
                       int32_t* step_counts, int32_t* iters, hjcd_stream_t stream);
+
+/* hjcd_pjik that also records every seed's decision at every iteration
+ * (parity testing: the oracle replays these decisions in fp64).
+ *   trace [T][B][lm_iters] out, device, caller-owned; one word per
+ *   (target, polish slot, iteration k) at which that seed took a step
+ *   (words past a seed's iteration count, and slots >= floor(B/K)*K, are left
+ *   unwritten):
+ *   bits 0-1 the branch that moved the seed: 0 the LM step (Alg. 4 l.3-9,
+ *   Eq. 12-13), 1 the dogleg step (l.10-12, Eqs. 14-15), 2 the
+ *   single-coordinate step (l.13-16, Eq. 16), 3 the perturbation (l.17);
+ *   bits 2-6 the line-search index a (step beta^-a; 0 for dogleg and
+ *   perturbation); bits 8-12 the single-coordinate index i* (branch 2 only);
+ *   bit 15 set (a step was taken).
+ *   theta_hist [T][B][lm_iters + 1][dof] out (device) or NULL: each seed's
+ *   theta at the start of every iteration it ran, as in hjcd_poccd_trace.
+ *   Same errors as hjcd_pjik. */
+hjcd_status hjcd_pjik_trace(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                            const float* seeds, float* theta, float* pos_err, float* ori_err,
+                            int32_t* step_counts, int32_t* iters, uint32_t* trace, float* theta_hist,
+                            hjcd_stream_t stream);
 
 /* Best-of-B selection (Alg. 2 l.9-10, R27): fine-converged seeds first, then
  * argmin_b w_p^2 pe^2 + w_o^2 oe^2, ties -> lowest b; writes

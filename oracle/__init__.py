@@ -77,10 +77,10 @@ def lib():
         _lib.oracle_fk.argtypes = [P, P, i32, P, P, P, P]
         _lib.oracle_po_ccd.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P, P]
         _lib.oracle_ccd.argtypes = [P, P, P, i32, i64, P, P, P, P]
-        _lib.oracle_po_ccd_replay.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P, P]
+        _lib.oracle_po_ccd_replay.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P, P, P, P]
         _lib.oracle_select_replicate.argtypes = [P, P, P, P, i32, i64, P, P]
         _lib.oracle_pj_ik.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P, P]
-        _lib.oracle_pj_ik_replay.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P, P, P, P]
+        _lib.oracle_pj_ik_replay.argtypes = [P, P, P, i32, i64, P, P, P, P, P, P, P, P, P, P, P, P]
         _lib.oracle_solve.argtypes = [P, P, P, i32, i64, P, P, P, P]
         _lib.oracle_line_search.argtypes = [P, P, P, P, P]
         _lib.oracle_lm_step.argtypes = [P, P, i32, P, P, P]
@@ -88,6 +88,8 @@ def lib():
         _lib.oracle_single_coord_step.argtypes = [P, P, i32, P, P, P]
         _lib.oracle_weights.argtypes = [P, P, i32, P]
         _lib.oracle_num_threads.restype = C.c_int
+        _lib.oracle_set_num_threads.argtypes = [i32]
+        _lib.oracle_set_num_threads.restype = None
     return _lib
 
 
@@ -265,12 +267,18 @@ def po_ccd(chain, params, targets, tid_offset: int = 0, seeds: Optional[np.ndarr
     return out
 
 
-def po_ccd_replay(chain, params, targets, trace, iters, tid_offset: int = 0):
+def po_ccd_replay(chain, params, targets, trace, iters, tid_offset: int = 0, theta_hist=None):
     """Alg. 3 in fp64 following recorded decisions (hjcd_poccd_trace words,
     trace [T,M,ccd_iters] uint32, iters [T,M]) -> dict theta [T,n,M], ep, eo,
     gap [T,M] (how much worse any recorded decision is than the fp64 one) and
     stop_gap [T] (how far outside the coarse box the GPU stopped), gap_at [T,M]
-    (8 k + kind of the largest gap: 1 jp, 2 jo, 3 same joint, 4 gamma, 5 stop; -1 none)."""
+    (8 k + kind of the largest gap: 1 jp, 2 jo, 3 same joint, 4 gamma, 5 stop; -1 none).
+    theta_hist [T,M,ccd_iters+1,n] f32 (hjcd_poccd_trace history) resynchronises
+    every iteration on the GPU's state (each decision also judged at states one
+    fp32 ulp away; the smallest gap counts) and adds step_dev [T,M] (largest
+    one-step difference, task space: end-effector m / rotation rad),
+    step_excess (its excess over 10x the spread of the fp64 steps from the
+    ulp-perturbed states) and step_dev_joint (max |dtheta_j|)."""
     r, c = make_robot(chain), make_config(params)
     tg = np.ascontiguousarray(targets, dtype=np.float32).reshape(-1, 7)
     T, n, M = tg.shape[0], chain.dof, params["M"]
@@ -278,9 +286,15 @@ def po_ccd_replay(chain, params, targets, trace, iters, tid_offset: int = 0):
     it = np.ascontiguousarray(iters, dtype=np.int32).reshape(T, M)
     out = dict(theta=np.empty((T, n, M)), ep=np.empty((T, M)), eo=np.empty((T, M)),
                gap=np.empty((T, M)), stop_gap=np.empty(T), gap_at=np.empty((T, M), dtype=np.int32))
+    h = None
+    if theta_hist is not None:
+        h = np.ascontiguousarray(theta_hist, dtype=np.float32).reshape(T, M, params["ccd_iters"] + 1, n)
+        sd = np.zeros((T, M, 3))
     lib().oracle_po_ccd_replay(_ref(r), _ref(c), _p(tg), T, tid_offset, _p(tr), _p(it), _p(out["theta"]),
                                _p(out["ep"]), _p(out["eo"]), _p(out["gap"]), _p(out["stop_gap"]),
-                               _p(out["gap_at"]))
+                               _p(out["gap_at"]), _p(h), _p(sd if h is not None else None))
+    if h is not None:
+        out["step_dev"], out["step_excess"], out["step_dev_joint"] = (sd[..., i].copy() for i in range(3))
     return out
 
 
@@ -339,13 +353,16 @@ def pj_word_fields(w):
     return w & 3, (w >> 2) & 31, (w >> 8) & 31, (w >> 15) & 1
 
 
-def pj_ik_replay(chain, params, targets, seeds, trace, iters, tid_offset: int = 0):
+def pj_ik_replay(chain, params, targets, seeds, trace, iters, tid_offset: int = 0, theta_hist=None):
     """Alg. 4 in fp64 following recorded decisions (hjcd_pjik_trace words,
     trace [T,B,lm_iters] uint32, iters [T,B]) -> dict theta [T,B,n], ep, eo,
     counts [T,B,4], gap [T,B] (how much worse any recorded decision is than the
     fp64 one, residual-norm units), stop_gap [T], gap_at [T,B] (8 k + kind:
     1 LM trial, 2 dogleg, 3 single index, 4 single trial, 5 continued inside the
-    fine box, 6 invalid word; -1 none)."""
+    fine box, 6 invalid word; -1 none).  theta_hist [T,B,lm_iters+1,n] f32
+    (hjcd_pjik_trace history) resynchronises every iteration on the GPU's
+    state and adds step_dev, step_excess and step_dev_joint [T,B] as
+    po_ccd_replay."""
     r, c = make_robot(chain), make_config(params)
     tg = np.ascontiguousarray(targets, dtype=np.float32).reshape(-1, 7)
     sd = np.ascontiguousarray(seeds, dtype=np.float64)
@@ -356,9 +373,15 @@ def pj_ik_replay(chain, params, targets, seeds, trace, iters, tid_offset: int = 
     out = dict(theta=np.full((T, B, n), np.nan), ep=np.full((T, B), np.nan), eo=np.full((T, B), np.nan),
                counts=np.zeros((T, B, 4), dtype=np.int32), gap=np.zeros((T, B)), stop_gap=np.empty(T),
                gap_at=np.full((T, B), -1, dtype=np.int32))
+    h = None
+    if theta_hist is not None:
+        h = np.ascontiguousarray(theta_hist, dtype=np.float32).reshape(T, B, I + 1, n)
+        dev = np.zeros((T, B, 3))
     lib().oracle_pj_ik_replay(_ref(r), _ref(c), _p(tg), T, tid_offset, _p(sd), _p(tr), _p(it), _p(out["theta"]),
                               _p(out["ep"]), _p(out["eo"]), _p(out["counts"]), _p(out["gap"]),
-                              _p(out["stop_gap"]), _p(out["gap_at"]))
+                              _p(out["stop_gap"]), _p(out["gap_at"]), _p(h), _p(dev if h is not None else None))
+    if h is not None:
+        out["step_dev"], out["step_excess"], out["step_dev_joint"] = (dev[..., i].copy() for i in range(3))
     return out
 
 
@@ -418,3 +441,8 @@ def mmd2(X, Y):
 
 def num_threads() -> int:
     return lib().oracle_num_threads()
+
+
+def set_num_threads(k: int) -> None:
+    """OpenMP threads of the oracle's loops (results do not depend on it)."""
+    lib().oracle_set_num_threads(int(k))

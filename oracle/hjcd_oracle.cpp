@@ -485,7 +485,15 @@ void po_ccd_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint
         if (forced) {
             dpa[j] = dp[j]; spa[j] = sp[j];
             if (r->type[ent] == 0 && stepp != 0.0) {
-                tp[j] = std::min(PI - std::fabs(stepp), std::fabs(stepp));
+                /* the sign of Eq. 9's step is the sign of y = z.(u_p x v_p) =
+                 * |u_p||v_p| sin(step): both of its ties (a vanishing step, and
+                 * the +-pi branch cut) are y = 0, and a float evaluation of y
+                 * errs by ~eps |u||v| (u = P_ee - P_j, v = P_t - P_j), so the
+                 * tie distance is |y| / (|u||v|) */
+                V3 u = sub(F.pee, F.P[j]), v = sub(tgt.p, F.P[j]);
+                double rr = dot(F.z[j], F.z[j]);
+                V3 up = sub(u, scl(F.z[j], dot(u, F.z[j]) / rr)), vp = sub(v, scl(F.z[j], dot(v, F.z[j]) / rr));
+                tp[j] = std::fabs(std::sin(stepp)) * norm(up) * norm(vp) / (norm(u) * norm(v));
                 dpa[j] = clampd(th[j] - stepp, lo, hi) - th[j];
                 thc = th; thc[j] = th[j] + dpa[j];
                 fk(rb, thc.data(), Fc);
@@ -703,6 +711,32 @@ void uniform_seed(const Robot& rb, uint64_t seed, uint64_t tid, uint32_t sid, do
     }
 }
 
+/* splitmix64 stream (replay variants only; the method's own draws are Philox) */
+uint64_t splitmix64(uint64_t& x) {
+    uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+/* u * 2^-23, u uniform in [-1, 1]: one fp32 rounding's relative size */
+double ulp32_noise(uint64_t& st) {
+    return ((double)(splitmix64(st) >> 11) * (2.0 / 9007199254740992.0) - 1.0) * std::ldexp(1.0, -23);
+}
+
+/* replay variants only (rng != NULL): every entry of a symmetric n x n matrix
+ * scaled by (1 + one fp32 rounding), the size of the error a float
+ * accumulation of its sums carries (the normal matrices of Eq. 12 and Eq. 14
+ * can be ill-conditioned enough for that to matter) */
+void perturb_sym(std::vector<double>& H, int n, uint64_t* rng) {
+    if (!rng) return;
+    for (int a = 0; a < n; ++a)
+        for (int b = a; b < n; ++b) {
+            double v = H[a * n + b] * (1.0 + ulp32_noise(*rng));
+            H[a * n + b] = H[b * n + a] = v;
+        }
+}
+
 /* ---------------- dense SPD solve (Cholesky), n x n ---------------- */
 bool cholesky_solve(std::vector<double> A, int n, const double* b, double* x) {
     /* A = L L^T in place (lower) */
@@ -730,6 +764,33 @@ bool cholesky_solve(std::vector<double> A, int n, const double* b, double* x) {
         x[i] = s / A[i * n + i];
     }
     return true;
+}
+
+/* replay resynchronisation: the end-effector distance (m) and rotation angle
+ * (rad) between FK(a) and FK(b): one step's fp32-vs-fp64 difference measured
+ * where it matters (a joint whose axis passes near the end effector can differ
+ * in angle without moving it) */
+double task_distance(const Robot& rb, const double* a, const double* b) {
+    Frames Fa, Fb;
+    fk(rb, a, Fa);
+    fk(rb, b, Fb);
+    return std::max(norm(sub(Fa.pee, Fb.pee)), norm(quat_error(Fa.qee, Fb.qee)));
+}
+
+/* replay resynchronisation: the states "one fp32 ulp away" from theta_k at
+ * which a recorded decision is also judged (a float evaluation cannot tell
+ * them apart): every joint moved by u * 2^-23 * max(|theta_j|, 1 rad or m),
+ * u uniform in [-1, 1] from a splitmix64 stream keyed by (seed row, k,
+ * variant), then clamped into the limits */
+const int REPLAY_VARIANTS = 4;
+const double REPLAY_SPREAD_FACTOR = 10.0;
+
+void perturb_ulp(const Robot& rb, std::vector<double>& th, uint64_t key) {
+    uint64_t st = key;
+    for (int j = 0; j < rb.dof; ++j) {
+        int ent = rb.dof_entry[j];
+        th[j] = clampd(th[j] + ulp32_noise(st) * std::max(std::fabs(th[j]), 1.0), rb.r->lo[ent], rb.r->hi[ent]);
+    }
 }
 
 /* ---------------- PJ-IK pieces (Alg. 4) ---------------- */
@@ -763,7 +824,7 @@ double norm6(const double v[6]) {
 /* Eq. 12 with the missing W restored (R18), D = max(diag(J^T J),
  * d_floor) (R20): (J^T W^2 J + lambda D) dtheta = -J^T W^2 rho, literal n x n. */
 bool lm_step(const OracleConfig& c, const double* J, int n, const double W[6],
-             const double rho[6], double* dth) {
+             const double rho[6], double* dth, uint64_t* rng = nullptr) {
     std::vector<double> H(n * n, 0.0), g(n, 0.0);
     for (int a = 0; a < n; ++a) {
         for (int b = 0; b < n; ++b) {
@@ -778,6 +839,7 @@ bool lm_step(const OracleConfig& c, const double* J, int n, const double W[6],
         for (int i = 0; i < 6; ++i) s += J[i * n + a] * W[i] * W[i] * rho[i];
         g[a] = -s;
     }
+    perturb_sym(H, n, rng);
     return cholesky_solve(H, n, g.data(), dth);
 }
 
@@ -785,7 +847,8 @@ bool lm_step(const OracleConfig& c, const double* J, int n, const double W[6],
  * GN = -(J^T J + d_floor I)^-1 J^T rho, dtheta(tau) = tau GD + (1-tau) GN with
  * the smallest tau in [0,1] such that |dtheta(tau)| <= R; none -> GD scaled to
  * |.| = R.  Returns false on a zero gradient. */
-bool dogleg_step(const OracleConfig& c, const double* J, int n, const double rho[6], double* dth) {
+bool dogleg_step(const OracleConfig& c, const double* J, int n, const double rho[6], double* dth,
+                 uint64_t* rng = nullptr) {
     std::vector<double> g0(n, 0.0);
     double gg = 0;
     for (int a = 0; a < n; ++a) {
@@ -815,6 +878,7 @@ bool dogleg_step(const OracleConfig& c, const double* J, int n, const double rho
         H[a * n + a] += c.d_floor;
         rhs[a] = -g0[a];
     }
+    perturb_sym(H, n, rng);
     if (!cholesky_solve(H, n, rhs.data(), gn.data())) return false;
     double ngn2 = 0;
     for (int a = 0; a < n; ++a) ngn2 += gn[a] * gn[a];
@@ -1000,7 +1064,7 @@ void pj_ik_step(const Robot& rb, const OracleConfig& c, const Target& tgt, uint6
  * single-coordinate trial, 6 an invalid word. */
 void pj_ik_step_replay(const Robot& rb, const OracleConfig& c, const Target& tgt, uint64_t tid,
                        uint32_t bidx, int k, const Frames& F, const Err& e, std::vector<double>& th,
-                       PolishOut& po, uint32_t word, double* gap, int* gap_kind) {
+                       PolishOut& po, uint32_t word, double* gap, int* gap_kind, uint64_t* rng = nullptr) {
     const OracleRobot* r = rb.r;
     int n = rb.dof;
     auto upd = [&](double g, int kind) { if (g > *gap) { *gap = g; *gap_kind = kind; } };
@@ -1028,7 +1092,7 @@ void pj_ik_step_replay(const Robot& rb, const OracleConfig& c, const Target& tgt
     };
     auto depth = [&](double ct) { return std::fabs(std::sqrt(2.0 * ct) - std::sqrt(2.0 * c0)); };
     /* LM line search (l.3-9): items alpha_0 .. alpha_A */
-    bool lm_ok = lm_step(c, J.data(), n, W, rho, dth.data());
+    bool lm_ok = lm_step(c, J.data(), n, W, rho, dth.data(), rng);
     if (lm_ok)
         for (int j = 0; j < n; ++j) dth[j] = clampd(dth[j], -c.R, c.R);
     double alpha = 1.0;
@@ -1048,7 +1112,7 @@ void pj_ik_step_replay(const Robot& rb, const OracleConfig& c, const Target& tgt
     }
     /* dogleg (l.10-12) */
     std::vector<double> dd(n);
-    if (dogleg_step(c, J.data(), n, rho, dd.data())) {
+    if (dogleg_step(c, J.data(), n, rho, dd.data(), rng)) {
         trial_point(rb, th, dd.data(), 1.0, tt);
         fk(rb, tt.data(), Ft);
         Err et = residual(Ft, tgt);
@@ -1369,11 +1433,26 @@ void oracle_po_ccd(const OracleRobot* r, const OracleConfig* c, const float* tar
  *   stop_gap [T]: the distance outside the coarse box of the seed closest to
  *     it where the GPU stopped before ccd_iters (per target with
  *     ccd_early_exit, else the max over the seeds of their own); 0 if none.
- * theta f64 [T][n][M], ep/eo f64 [T][M] after the replay. */
+ * theta f64 [T][n][M], ep/eo f64 [T][M] after the replay.
+ * theta_hist f32 [T][M][ccd_iters + 1][n] or NULL: the GPU's theta at the
+ *   start of every iteration (hjcd_poccd_trace).  Given, the replay is
+ *   RESYNCHRONISED: iteration k starts from the GPU's theta_k instead of this
+ *   oracle's own continuation, so every decision is judged at the exact state
+ *   the GPU took it in and fp32 drift cannot accumulate.  A decision is also
+ *   judged at REPLAY_VARIANTS states one fp32 ulp away from theta_k
+ *   (perturb_ulp), and the smallest gap counts: fp32 cannot tell those states
+ *   apart.  step_dev [T][M][3] (or NULL) receives, over k, (0) the largest
+ *   task-space difference (task_distance: end-effector m / rotation rad)
+ *   between this oracle's fp64 step from theta_k and the GPU's theta_{k+1}
+ *   (one step's fp32-vs-fp64 difference under identical decisions), (1) the
+ *   largest excess of that difference over REPLAY_SPREAD_FACTOR x the spread
+ *   of the fp64 steps from the ulp-perturbed states (how well fp32 can
+ *   determine the step at all: a step near a joint axis or a singular
+ *   Jacobian is ill-conditioned), (2) the largest max_j |dtheta_j|. */
 void oracle_po_ccd_replay(const OracleRobot* r, const OracleConfig* c, const float* targets, int32_t T,
                           int64_t tid_offset, const uint32_t* trace, const int32_t* iters,
                           double* theta, double* ep, double* eo, double* gap, double* stop_gap,
-                          int32_t* gap_at) {
+                          int32_t* gap_at, const float* theta_hist, double* step_dev) {
     Robot rb = make_robot(r);
     int n = rb.dof, M = c->M, I = c->ccd_iters;
 #pragma omp parallel for schedule(dynamic, 1)
@@ -1389,9 +1468,20 @@ void oracle_po_ccd_replay(const OracleRobot* r, const OracleConfig* c, const flo
             SeedOut so = seed_init();
             Frames F;
             Err e;
-            double g = 0.0;
+            double g = 0.0, sd = 0.0, sdj = 0.0, sdx = -INF, spread = 0.0;
             int K = iters[o], kind = 0, at = -1;
             for (int k = 0;; ++k) {
+                if (theta_hist && k <= I) {   /* resynchronise on the GPU's theta_k */
+                    const float* h = theta_hist + (o * (size_t)(I + 1) + k) * n;
+                    std::vector<double> hk(h, h + n);
+                    if (k > 0) {
+                        double dv = task_distance(rb, th.data(), hk.data());
+                        sd = std::max(sd, dv);
+                        sdx = std::max(sdx, dv - REPLAY_SPREAD_FACTOR * spread);
+                        for (int j = 0; j < n; ++j) sdj = std::max(sdj, std::fabs(th[j] - hk[j]));
+                    }
+                    th = hk;
+                }
                 po_ccd_check(rb, *c, tgt, th, F, e, so);
                 double inside = std::min(c->eps_p_coarse - e.ep, c->eps_o_coarse - e.eo);
                 if (k == K) {
@@ -1403,10 +1493,31 @@ void oracle_po_ccd_replay(const OracleRobot* r, const OracleConfig* c, const flo
                     break;
                 }
                 if (inside > g) { g = inside; at = 8 * k + 5; }
+                const uint32_t* w = trace + o * I + k;
+                std::vector<double> thk = th;
+                double gk = 0.0;
                 kind = 0;
-                double g0 = g;
-                po_ccd_step(rb, *c, tgt, tid, (uint32_t)m, k, F, e, th, so, trace + o * I + k, &g, nullptr, &kind);
-                if (g > g0) at = 8 * k + kind;
+                po_ccd_step(rb, *c, tgt, tid, (uint32_t)m, k, F, e, th, so, w, &gk, nullptr, &kind);
+                spread = 0.0;
+                if (theta_hist) {
+                    /* the same decision one fp32 ulp away: the smallest gap over
+                     * the variants counts, and the spread of their results
+                     * measures how well fp32 can determine this step */
+                    for (int v = 1; v <= REPLAY_VARIANTS; ++v) {
+                        std::vector<double> tv = thk;
+                        perturb_ulp(rb, tv, (o * 1024 + (uint64_t)k) * 8 + (uint64_t)v);
+                        Frames Fv;
+                        Err ev;
+                        SeedOut sov = seed_init();
+                        po_ccd_check(rb, *c, tgt, tv, Fv, ev, sov);
+                        double gv = 0.0;
+                        int kv = 0;
+                        po_ccd_step(rb, *c, tgt, tid, (uint32_t)m, k, Fv, ev, tv, sov, w, &gv, nullptr, &kv);
+                        if (gv < gk) { gk = gv; kind = kv; }
+                        spread = std::max(spread, task_distance(rb, th.data(), tv.data()));
+                    }
+                }
+                if (gk > g) { g = gk; at = 8 * k + kind; }
                 if (!std::isfinite(g)) break;
             }
             for (int j = 0; j < n; ++j) theta[((size_t)t * n + j) * M + m] = th[j];
@@ -1414,6 +1525,7 @@ void oracle_po_ccd_replay(const OracleRobot* r, const OracleConfig* c, const flo
             eo[o] = so.eo;
             gap[o] = g;
             if (gap_at) gap_at[o] = at;
+            if (step_dev) { step_dev[3 * o] = sd; step_dev[3 * o + 1] = sdx; step_dev[3 * o + 2] = sdj; }
         }
         stop_gap[t] = stopped ? sg : 0.0;
     }
@@ -1520,11 +1632,18 @@ void oracle_pj_ik(const OracleRobot* r, const OracleConfig* c, const float* targ
  *     where the GPU stopped before lm_iters (per target with
  *     target_early_exit, else the max over the seeds of their own); 0 if none.
  * theta f64 [T][B][n], ep/eo f64 [T][B], counts i32 [T][B][4] after the replay
- * (slots >= floor(B/K) K untouched). */
+ * (slots >= floor(B/K) K untouched).
+ * theta_hist f32 [T][B][lm_iters + 1][n] or NULL: the GPU's theta at the
+ *   start of every iteration (hjcd_pjik_trace); given, the replay is
+ *   resynchronised on it at every iteration, judged also one ulp away (here
+ *   the variants also carry one fp32 rounding in every entry of the normal
+ *   matrices of the LM and dogleg solves, perturb_sym), and step_dev
+ *   [T][B][3] (or NULL) receives the one-step differences, as in
+ *   oracle_po_ccd_replay. */
 void oracle_pj_ik_replay(const OracleRobot* r, const OracleConfig* c, const float* targets, int32_t T,
                          int64_t tid_offset, const double* seeds, const uint32_t* trace, const int32_t* iters,
                          double* theta, double* ep, double* eo, int32_t* counts, double* gap,
-                         double* stop_gap, int32_t* gap_at) {
+                         double* stop_gap, int32_t* gap_at, const float* theta_hist, double* step_dev) {
     Robot rb = make_robot(r);
     int n = rb.dof, B = c->B, I = c->lm_iters;
     int used = (c->B / c->K) * c->K;
@@ -1540,9 +1659,20 @@ void oracle_pj_ik_replay(const OracleRobot* r, const OracleConfig* c, const floa
             PolishOut po = polish_init();
             Frames F;
             Err e;
-            double g = 0.0;
+            double g = 0.0, sd = 0.0, sdj = 0.0, sdx = -INF, spread = 0.0;
             int K = iters[o], kind = 0, at = -1;
             for (int k = 0;; ++k) {
+                if (theta_hist && k <= I) {   /* resynchronise on the GPU's theta_k */
+                    const float* h = theta_hist + (o * (size_t)(I + 1) + k) * n;
+                    std::vector<double> hk(h, h + n);
+                    if (k > 0) {
+                        double dv = task_distance(rb, th.data(), hk.data());
+                        sd = std::max(sd, dv);
+                        sdx = std::max(sdx, dv - REPLAY_SPREAD_FACTOR * spread);
+                        for (int j = 0; j < n; ++j) sdj = std::max(sdj, std::fabs(th[j] - hk[j]));
+                    }
+                    th = hk;
+                }
                 pj_ik_check(rb, *c, tgt, th, F, e, po);
                 double inside = std::min(c->eps_p_fine - e.ep, c->eps_o_fine - e.eo);
                 if (k == K) {
@@ -1555,9 +1685,29 @@ void oracle_pj_ik_replay(const OracleRobot* r, const OracleConfig* c, const floa
                 }
                 if (k >= I) { g = INF; at = 8 * k + 6; break; }   /* more iterations than the budget */
                 if (inside > g) { g = inside; at = 8 * k + 5; }
-                double g0 = g;
-                pj_ik_step_replay(rb, *c, tgt, tid, (uint32_t)b, k, F, e, th, po, trace[o * I + k], &g, &kind);
-                if (g > g0) at = 8 * k + kind;
+                const uint32_t w = trace[o * I + k];
+                std::vector<double> thk = th;
+                double gk = 0.0;
+                kind = 0;
+                pj_ik_step_replay(rb, *c, tgt, tid, (uint32_t)b, k, F, e, th, po, w, &gk, &kind);
+                spread = 0.0;
+                if (theta_hist) {   /* as in oracle_po_ccd_replay */
+                    for (int v = 1; v <= REPLAY_VARIANTS; ++v) {
+                        std::vector<double> tv = thk;
+                        perturb_ulp(rb, tv, (o * 1024 + (uint64_t)k) * 8 + (uint64_t)v);
+                        Frames Fv;
+                        Err ev;
+                        PolishOut pov = polish_init();
+                        pj_ik_check(rb, *c, tgt, tv, Fv, ev, pov);
+                        double gv = 0.0;
+                        int kv = 0;
+                        uint64_t nrng = ((o * 1024 + (uint64_t)k) * 8 + (uint64_t)v) ^ 0x5bd1e995ull;
+                        pj_ik_step_replay(rb, *c, tgt, tid, (uint32_t)b, k, Fv, ev, tv, pov, w, &gv, &kv, &nrng);
+                        if (gv < gk) { gk = gv; kind = kv; }
+                        spread = std::max(spread, task_distance(rb, th.data(), tv.data()));
+                    }
+                }
+                if (gk > g) { g = gk; at = 8 * k + kind; }
                 if (!std::isfinite(g)) break;
             }
             for (int j = 0; j < n; ++j) theta[o * n + j] = th[j];
@@ -1566,6 +1716,7 @@ void oracle_pj_ik_replay(const OracleRobot* r, const OracleConfig* c, const floa
             if (counts) for (int i = 0; i < 4; ++i) counts[o * 4 + i] = po.counts[i];
             gap[o] = g;
             if (gap_at) gap_at[o] = at;
+            if (step_dev) { step_dev[3 * o] = sd; step_dev[3 * o + 1] = sdx; step_dev[3 * o + 2] = sdj; }
         }
         stop_gap[t] = stopped ? sg : 0.0;
     }
@@ -1639,6 +1790,15 @@ void oracle_solve(const OracleRobot* r, const OracleConfig* c, const float* targ
         else if (bep < c->succ_p && beo < c->succ_o) status[t] = 1;
         else status[t] = 2;
     }
+}
+
+/* host threads for the OpenMP loops (bench.py's cpu_baseline times 1 and all) */
+void oracle_set_num_threads(int32_t k) {
+#ifdef _OPENMP
+    if (k > 0) omp_set_num_threads(k);
+#else
+    (void)k;
+#endif
 }
 
 int oracle_num_threads(void) {

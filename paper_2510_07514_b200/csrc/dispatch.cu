@@ -15,7 +15,7 @@ int poccd_nmax(int n) {   // must match launch_poccd's choice below
 
 cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                          const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                         int32_t* iters, cudaStream_t s, uint32_t* trace, uint32_t* ready) {
+                         int32_t* iters, cudaStream_t s, TraceOut trace, uint32_t* ready) {
     switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
         case 7: return launch_poccd_t<7, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
         case 8: return launch_poccd_t<8, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);

@@ -4,8 +4,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "hjcd_internal.h"
@@ -225,6 +227,66 @@ hjcd_status check_poccd(const hjcd_config* c) {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// One solve at a time per workspace (hjcd.h): the host remembers, per workspace
+// address, the stream of its last solve and an event recorded after that
+// solve's launches.  A solve on ANOTHER stream while that event is pending
+// would share the stage-1 buffers and readiness counts of a solve in flight;
+// it is refused with HJCD_E_WORKSPACE instead of racing (or, in the dependent
+// launch, waiting on counts the other solve resets).  The same stream is
+// stream-ordered and always allowed; graph capture is left to the caller.
+struct WsUse {
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev = nullptr;
+    int dev = -1;
+};
+std::mutex g_ws_mu;
+std::unordered_map<const void*, WsUse> g_ws;
+
+bool capturing(cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return cs != cudaStreamCaptureStatusNone;
+}
+
+hjcd_status ws_acquire(const void* ws, cudaStream_t s) {
+    if (capturing(s)) return HJCD_OK;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto it = g_ws.find(ws);
+    if (it == g_ws.end() || it->second.s == s || !it->second.ev) return HJCD_OK;
+    cudaError_t e = cudaEventQuery(it->second.ev);
+    if (e == cudaErrorNotReady) return HJCD_E_WORKSPACE;
+    if (e != cudaSuccess) (void)cudaGetLastError();
+    return HJCD_OK;
+}
+
+void ws_release(const void* ws, cudaStream_t s) {
+    if (capturing(s)) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { (void)cudaGetLastError(); return; }
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    WsUse& u = g_ws[ws];
+    if (u.ev && u.dev != dev) { cudaEventDestroy(u.ev); u.ev = nullptr; }
+    if (!u.ev && cudaEventCreateWithFlags(&u.ev, cudaEventDisableTiming) != cudaSuccess) {
+        (void)cudaGetLastError();
+        u.ev = nullptr;
+        return;
+    }
+    u.dev = dev;
+    u.s = s;
+    if (cudaEventRecord(u.ev, s) != cudaSuccess) (void)cudaGetLastError();
+}
+
+// acquired for the scope of one solve's launches; marks the workspace busy on
+// `s` until the work enqueued in that scope completes
+struct WsScope {
+    const void* ws;
+    cudaStream_t s;
+    ~WsScope() { ws_release(ws, s); }
+};
+
 struct Layout {
     size_t theta1, cost1, seeds2, ep2, eo2, ready, total;
 };
@@ -281,6 +343,7 @@ cudaError_t solve_linked(const hjcd_robot* r, const DevCfg& d, const float* targ
     int nt, CL;
     texit_shape(d.M, poccd_nmax(r->dof), nt, CL);
     link.need = (uint32_t)CL;
+    link.spin_limit = (1ull << 26) * (unsigned long long)(1 + d.ccd_iters / 64);
     link.Mpad = 2;
     while (link.Mpad < d.M) link.Mpad <<= 1;
 #ifdef HJCD_PROBE
@@ -291,7 +354,7 @@ cudaError_t solve_linked(const hjcd_robot* r, const DevCfg& d, const float* targ
         return e;
 #endif
     if ((e = cudaMemsetAsync(link.ready, 0, (size_t)T * sizeof(uint32_t), s)) != cudaSuccess ||
-        (e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s, nullptr,
+        (e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s, TraceOut(),
                           link.ready)) != cudaSuccess ||
         (e = launch_pjik(r->dev, d, targets, T, nullptr, seeds2, ep2, eo2, nullptr, nullptr, s, link)) != cudaSuccess)
         return e;
@@ -340,11 +403,17 @@ hjcd_status hjcd_robot_extend(const hjcd_robot* r, int32_t target_dof, hjcd_robo
     if (!r || !out) return HJCD_E_INVALID_ARG;
     if (target_dof < r->dof) return HJCD_E_INVALID_ARG;
     if (target_dof > HJCD_MAX_DOF) return HJCD_E_UNSUPPORTED;
-    std::vector<hjcd_joint> base, all = r->joints;
+    // cyclic replicas of the DoF joints (R34) go before the end-effector
+    // offset, which includes any trailing run of FIXED joints (SPEC extend_dof)
+    std::vector<hjcd_joint> base;
     for (const hjcd_joint& j : r->joints)
         if (j.type != HJCD_FIXED) base.push_back(j);
+    size_t tail = r->joints.size();
+    while (tail > 0 && r->joints[tail - 1].type == HJCD_FIXED) --tail;
+    std::vector<hjcd_joint> all(r->joints.begin(), r->joints.begin() + tail);
     int d = r->dof;
     for (size_t i = 0; d < target_dof; ++i, ++d) all.push_back(base[i % base.size()]);
+    all.insert(all.end(), r->joints.begin() + tail, r->joints.end());
     return build_robot(all.data(), (int32_t)all.size(), r->ee_xyz, r->ee_quat, out);
 }
 
@@ -422,6 +491,8 @@ hjcd_status hjcd_solve_timed(const hjcd_robot* r, const hjcd_config* c, const fl
     float* ep2 = (float*)(ws + L.ep2);
     float* eo2 = (float*)(ws + L.eo2);
     cudaStream_t s = (cudaStream_t)stream;
+    if ((st = ws_acquire(workspace, s)) != HJCD_OK) return st;
+    WsScope busy{workspace, s};
     cudaError_t e;
     auto mark = [&](int i) -> cudaError_t {
         return (events && events[i]) ? cudaEventRecord((cudaEvent_t)events[i], s) : cudaSuccess;
@@ -469,6 +540,8 @@ hjcd_status hjcd_solve_batch(const hjcd_robot* r, const hjcd_config* c, const fl
     if (workspace_bytes < L.total || ((uintptr_t)workspace & 255)) return HJCD_E_WORKSPACE;
     char* ws = (char*)workspace;
     cudaStream_t s = (cudaStream_t)stream;
+    if ((st = ws_acquire(workspace, s)) != HJCD_OK) return st;
+    WsScope busy{workspace, s};
     cudaError_t e = solve_linked(r, d, targets, T, L, ws, s, [&](const float* th, const float* ep, const float* eo) {
         return launch_select_topn(r->dev, d, targets, T, th, ep, eo, N, q_out, pos_err, ori_err, nullptr, status, s);
     });
@@ -505,6 +578,8 @@ hjcd_status hjcd_solve_f64(const hjcd_robot* r, const hjcd_config* c, const floa
     double* ep64 = (double*)(ws + L.ep64);
     double* eo64 = (double*)(ws + L.eo64);
     cudaStream_t s = (cudaStream_t)stream;
+    if ((st = ws_acquire(workspace, s)) != HJCD_OK) return st;
+    WsScope busy{workspace, s};
     cudaError_t e;
     // stage 1 and the hand-over in fp32 (PO-CCD only needs the coarse
     // tolerance), stage 2 and the answer in fp64 on the fp64 chain (f1)
@@ -569,6 +644,7 @@ hjcd_status hjcd_solve_host(const hjcd_robot* r, const hjcd_config* c, const flo
     float* oe = (float*)io;            io += align256((size_t)T * 4);
     int32_t* stt = (int32_t*)io;
     cudaStream_t s = (cudaStream_t)stream;
+    if ((st = ws_acquire(workspace, s)) != HJCD_OK) return st;
     cudaError_t e;
     if ((e = cudaMemcpyAsync(tg, targets_host, (size_t)T * 7 * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
         return cuda_fail(e);
@@ -587,6 +663,20 @@ hjcd_status hjcd_fk(const hjcd_robot* r, const float* q, int32_t N, float* pose7
                     hjcd_stream_t stream) {
     if (!r || !q || N < 1 || !pose7) return HJCD_E_INVALID_ARG;
     cudaError_t e = launch_fk(r->dev, q, N, pose7, jac, (cudaStream_t)stream);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+}
+
+hjcd_status hjcd_fk_sfu(const hjcd_robot* r, const float* q, int32_t N, float* pose7, float* jac,
+                        hjcd_stream_t stream) {
+    if (!r || !q || N < 1 || !pose7) return HJCD_E_INVALID_ARG;
+    cudaError_t e = launch_fk(r->dev, q, N, pose7, jac, (cudaStream_t)stream, true);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+}
+
+hjcd_status hjcd_pose_error_f64(const hjcd_robot* r, const float* q, const float* targets, int32_t N,
+                                double* pos_err, double* ori_err, hjcd_stream_t stream) {
+    if (!r || !q || !targets || N < 1 || !pos_err || !ori_err) return HJCD_E_INVALID_ARG;
+    cudaError_t e = launch_pose_error64(r->dev64, q, targets, N, pos_err, ori_err, (cudaStream_t)stream);
     return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
 }
 
@@ -615,14 +705,17 @@ hjcd_status hjcd_ccd(const hjcd_robot* r, const hjcd_config* c, const float* tar
 
 hjcd_status hjcd_poccd_trace(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
                              const float* seeds, float* theta, float* cost, float* pos_err, float* ori_err,
-                             int32_t* iters, uint32_t* trace, hjcd_stream_t stream) {
+                             int32_t* iters, uint32_t* trace, float* theta_hist, hjcd_stream_t stream) {
     if (!r || !c || !targets || T < 1 || !theta || !cost || !trace) return HJCD_E_INVALID_ARG;
     DevCfg d;
     hjcd_status st = make_cfg(r, c, &d);
     if (st != HJCD_OK) return st;
     if ((st = check_poccd(c)) != HJCD_OK) return st;
+    TraceOut tr;
+    tr.words = trace;
+    tr.theta = theta_hist;
     cudaError_t e = launch_poccd(r->dev, d, targets, T, seeds, theta, cost, pos_err, ori_err, iters,
-                                 (cudaStream_t)stream, trace);
+                                 (cudaStream_t)stream, tr);
     return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
 }
 
@@ -650,6 +743,22 @@ hjcd_status hjcd_pjik(const hjcd_robot* r, const hjcd_config* c, const float* ta
     return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
 }
 
+hjcd_status hjcd_pjik_trace(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
+                            const float* seeds, float* theta, float* pos_err, float* ori_err, int32_t* step_counts,
+                            int32_t* iters, uint32_t* trace, float* theta_hist, hjcd_stream_t stream) {
+    if (!r || !c || !targets || T < 1 || !seeds || !theta || !pos_err || !ori_err || !trace)
+        return HJCD_E_INVALID_ARG;
+    DevCfg d;
+    hjcd_status st = make_cfg(r, c, &d);
+    if (st != HJCD_OK) return st;
+    StageLink extra;
+    extra.trace = trace;
+    extra.trace_theta = theta_hist;
+    cudaError_t e = launch_pjik(r->dev, d, targets, T, seeds, theta, pos_err, ori_err, step_counts, iters,
+                                (cudaStream_t)stream, extra);
+    return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
+}
+
 hjcd_status hjcd_select_best(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
                              const float* theta, const float* pos_err_all, const float* ori_err_all, float* q_out,
                              float* pos_err, float* ori_err, int32_t* status, hjcd_stream_t stream) {
@@ -670,7 +779,7 @@ const char* hjcd_status_string(hjcd_status s) {
         case HJCD_E_INVALID_ARG: return "invalid argument";
         case HJCD_E_UNSUPPORTED: return "unsupported";
         case HJCD_E_CUDA: return "CUDA error";
-        case HJCD_E_WORKSPACE: return "workspace too small or misaligned";
+        case HJCD_E_WORKSPACE: return "workspace too small, misaligned, or in use on another stream";
         case HJCD_E_NOMEM: return "out of host memory";
     }
     return "unknown status";

@@ -52,6 +52,14 @@ struct DevCfg {
     int64_t tid_offset;
 };
 
+// Decision trace of the PO-CCD kernel (hjcd_poccd_trace): the decision word
+// of every seed-iteration [T][M][ccd_iters], and optionally theta at the start
+// of every iteration [T][M][ccd_iters + 1][n] (the replay resynchronises on it)
+struct TraceOut {
+    uint32_t* words = nullptr;
+    float* theta = nullptr;
+};
+
 // Dependent launch of PJ-IK on PO-CCD inside hjcd_solve (K10). With
 // ready != nullptr the PO-CCD lockstep kernel adds 1 to ready[t] (release, gpu
 // scope) when a CTA of target t's cluster has written its seeds, and the PJ-IK
@@ -64,6 +72,14 @@ struct StageLink {
     const float* theta = nullptr;  // stage-1 theta [T][n][M]
     uint32_t need = 0;             // CTAs per PO-CCD cluster
     int32_t Mpad = 0;              // M rounded up to a power of two >= 2
+    // readiness polls (~0.5 us apart) before a waiting PJ-IK CTA traps instead
+    // of hanging (a stage 1 that cannot complete); scaled with the PO-CCD budget
+    unsigned long long spin_limit = 0;
+    // not part of the link: PJ-IK decision words [T][B][lm_iters] and theta at
+    // the start of every iteration [T][B][lm_iters + 1][n], or nullptr
+    // (hjcd_pjik_trace; word format in include/hjcd.h), for any launch
+    uint32_t* trace = nullptr;
+    float* trace_theta = nullptr;
 };
 
 // seeds per CTA (nt) and CTAs per cluster (CL) of the PO-CCD lockstep launch:
@@ -115,7 +131,7 @@ enum : uint32_t { P_INIT = 1, P_PERTURB = 2, P_REPL = 3, P_PJPERT = 4 };
 template <int NMAX, bool EXACT>
 cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                            const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                           int32_t* iters, uint32_t* trace, uint32_t* ready, cudaStream_t s);
+                           int32_t* iters, TraceOut trace, uint32_t* ready, cudaStream_t s);
 template <int NMAX, bool EXACT>
 cudaError_t launch_ccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* seeds,
                          float* theta, float* ep, int32_t* iters, cudaStream_t s);
@@ -129,10 +145,10 @@ int poccd_nmax(int n);
 
 // launchers (dispatch.cu, select.cu); all asynchronous on `s`
 cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, float* jac,
-                      cudaStream_t s);
+                      cudaStream_t s, bool sfu = false);
 cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                          const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                         int32_t* iters, cudaStream_t s, uint32_t* trace = nullptr, uint32_t* ready = nullptr);
+                         int32_t* iters, cudaStream_t s, TraceOut trace = TraceOut(), uint32_t* ready = nullptr);
 cudaError_t launch_ccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T, const float* seeds,
                        float* theta, float* ep, int32_t* iters, cudaStream_t s);
 cudaError_t launch_select_replicate(const DevRobot& rb, const DevCfg& c, const float* cost,
@@ -154,6 +170,9 @@ template <class T>
 cudaError_t launch_select_best(const DevRobot& rb, const DevCfg& c, const float* targets, int T_,
                                const T* theta, const T* ep_all, const T* eo_all, T* q_out, T* pos_err,
                                T* ori_err, int32_t* status, cudaStream_t s);
+// fp64 pose error of fp32 configurations on the fp64 chain (hjcd_pose_error_f64)
+cudaError_t launch_pose_error64(const DevRobotT<double>& rb, const float* q, const float* targets, int N,
+                                double* pos_err, double* ori_err, cudaStream_t s);
 // fp64 polish: the same PJ-IK on DevRobotT<double>
 cudaError_t launch_pjik64(const DevRobotT<double>& rb, const DevCfg& c, const float* targets, int T,
                           const float* seeds, double* theta, double* ep, double* eo, int32_t* counts,

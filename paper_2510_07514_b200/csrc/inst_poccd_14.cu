@@ -2,5 +2,5 @@
 #include "poccd.cuh"
 
 namespace hjcd {
-template cudaError_t launch_poccd_t<14, true>(const DevRobot&, const DevCfg&, const float*, int, const float*, float*, float*, float*, float*, int32_t*, uint32_t*, uint32_t*, cudaStream_t);
+template cudaError_t launch_poccd_t<14, true>(const DevRobot&, const DevCfg&, const float*, int, const float*, float*, float*, float*, float*, int32_t*, TraceOut, uint32_t*, cudaStream_t);
 }  // namespace hjcd

@@ -98,12 +98,14 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
         if (b == 0) {
             const uint32_t* f = link.ready + t;
             uint32_t v;
-            for (uint32_t spins = 0;; ++spins) {
+            for (unsigned long long spins = 0;; ++spins) {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
                 if (v >= link.need) break;
-                // a stage 1 that cannot complete (e.g. one workspace shared by
-                // two solves in flight) becomes a CUDA error, not a hang (~30 s)
-                if (spins > (1u << 26)) __trap();
+                // a stage 1 that cannot complete becomes a CUDA error (the
+                // process's context is lost), not a hang: >= ~30 s of polling,
+                // scaled with ccd_iters, against ~ms for one PO-CCD cluster
+                // (every PO-CCD CTA is already resident when this grid starts)
+                if (spins > link.spin_limit) __trap();
                 __nanosleep(500);
             }
         }
@@ -150,6 +152,12 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
         vec3<T> pe;
         QuatT<T> qe;
         bool conv = false;
+        if (link.trace_theta && live) {   // theta at the start of iteration k (hjcd_pjik_trace)
+            float* h = link.trace_theta + (row * (c.lm_iters + 1) + k) * n;
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j)
+                if (EXACT || j < n) h[j] = (float)th[j];
+        }
         if (live) {
             fk<NMAX, true, EXACT, false, REV>(rb, th, Jp, Jo, pe, qe);
             r = residual(tg, pe, qe);
@@ -167,7 +175,8 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
         if (k == c.lm_iters) break;
 
         bool need = false, have_lm = false, accepted = false;
-        int flags = 0, items = 0;
+        int flags = 0, items = 0, ist = 0;
+        uint32_t word = 0u;   // hjcd_pjik_trace decision word of this iteration
         T W[6], c0 = T(0);
         if (live) {
             // ---- Eq. 7 Jacobian, W (R17), D (R20), c_W(theta), |rho|^2
@@ -229,7 +238,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
 #pragma unroll
                         for (int j = 0; j < NMAX; ++j) S.dir[(1 * NMAX + j) * nt + b] = dth[j];
                     }
-                    if (single_coord_direction<NMAX, EXACT>(rb, c, Jp, Jo, W, r.rho, dth)) {   // Eq. 16
+                    if (single_coord_direction<NMAX, EXACT>(rb, c, Jp, Jo, W, r.rho, dth, ist)) {   // Eq. 16
                         flags |= 4;
 #pragma unroll
                         for (int j = 0; j < NMAX; ++j) S.dir[(2 * NMAX + j) * nt + b] = dth[j];
@@ -259,7 +268,14 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
 #ifdef HJCD_PROBE2
                 p2_items += total;
 #endif
-                if (total == 0) break;   // uniform over the CTA
+                if (total == 0) {   // uniform over the CTA: no trial pending anywhere
+                    if (need) {     // every direction failed to form: Alg. 4 l.17 (R25)
+                        perturb<NMAX, EXACT, true>(rb, c, th, T(c.sigma_lm), tid, (uint32_t)b, P_PJPERT, (uint32_t)k);
+                        cnt[3]++;
+                        word = 3u | (1u << 15);
+                    }
+                    break;
+                }
                 // item -> (owner, index) table: each failing seed fills its range
                 for (int i = 0; i < items; ++i) {
                     S.own[incl - items + i] = (unsigned char)b;
@@ -321,6 +337,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                 if (own_ok) {
                     accepted = true;
                     cnt[0]++;
+                    word = 1u << 15;   // LM step, alpha index 0
 #pragma unroll
                     for (int j = 0; j < NMAX; ++j) th[j] = tt[j];
                 }
@@ -340,13 +357,16 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                         if (EXACT || j < n)
                             th[j] = clampf(th[j] + alpha * S.dir[(kind * NMAX + j) * nt + b], rb.j[j].lo, rb.j[j].hi);
                     cnt[kind]++;
+                    word = (uint32_t)kind | ((uint32_t)a << 2) | (kind == 2 ? (uint32_t)ist << 8 : 0u) | (1u << 15);
                 } else {
                     // R25; SFU Box-Muller in fp32 (K5: ~1e-6 relative on a sigma = 0.05 kick)
                     perturb<NMAX, EXACT, true>(rb, c, th, T(c.sigma_lm), tid, (uint32_t)b, P_PJPERT, (uint32_t)k);
                     cnt[3]++;
+                    word = 3u | (1u << 15);
                 }
             }
         }
+        if (link.trace && live) link.trace[row * c.lm_iters + k] = word;
         P2MARK(6);
     }
 #undef P2MARK

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(poccd_cta(NMAX), poccd_min_blocks<NMAX>() * 12
 k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float* __restrict__ targets, int T, const float* __restrict__ seeds,
         float* __restrict__ theta_out, float* __restrict__ cost_out, float* __restrict__ ep_out,
-        float* __restrict__ eo_out, int32_t* __restrict__ iters_out, int CL, uint32_t* __restrict__ trace,
+        float* __restrict__ eo_out, int32_t* __restrict__ iters_out, int CL, const TraceOut trace,
         uint32_t* __restrict__ ready) {
     const int M = c.M;
     const int n = rb.n;
@@ -107,6 +107,12 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     float rho_k = 1.f;   // delta_rho^k, by repeated multiplication (R5)
     int k;
     for (k = 0;; ++k, rho_k *= c.delta_rho) {
+        if (trace.theta && active) {   // theta at the start of iteration k (hjcd_poccd_trace)
+            float* h = trace.theta + (((long long)t * M + m) * (c.ccd_iters + 1) + k) * n;
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j)
+                if (EXACT || j < n) h[j] = th[j];
+        }
         fk<NMAX, true, EXACT, true, REV>(rb, th, P, Z, pe, qe);
         if constexpr (FRAMES_SMEM) {
             float2* s_fz = (float2*)(s_frames + NMAX * blockDim.x);
@@ -286,8 +292,8 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const float eo_h = 2.f * fast_atan2f(sqrtf(q2.x * q2.x + q2.y * q2.y + q2.z * q2.z), fabsf(q2.w));
         // ---- Alg. 3 l.11-13 (R10): accept on an improvement > gamma in either space
         const bool accept = (ep - ep_h) > c.gamma || (eo - eo_h) > c.gamma;
-        if (trace && active)   // decision word: see hjcd_poccd_trace (include/hjcd.h)
-            trace[((long long)t * M + m) * c.ccd_iters + k] =
+        if (trace.words && active)   // decision word: see hjcd_poccd_trace (include/hjcd.h)
+            trace.words[((long long)t * M + m) * c.ccd_iters + k] =
                 (uint32_t)jp | ((uint32_t)jo << 5) | ((jp == jo && db != dp_best) ? 1u << 10 : 0u) |
                 (accept ? 1u << 11 : 0u) | ((dp_best > 0.f ? 1u : dp_best < 0.f ? 2u : 0u) << 12) |
                 ((do_best > 0.f ? 1u : do_best < 0.f ? 2u : 0u) << 14);
@@ -370,7 +376,7 @@ inline size_t poccd_smem(int nt) {   // the per-thread frames (24 B per joint)
 template <int NMAX, bool EXACT, int REV>
 static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                                   const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                                  int32_t* iters, uint32_t* trace, uint32_t* ready, cudaStream_t s) {
+                                  int32_t* iters, TraceOut trace, uint32_t* ready, cudaStream_t s) {
     static std::atomic<unsigned long long> smem_attr{0};   // the frames copy may exceed the 48 KB default
     if (poccd_smem<NMAX>(poccd_cta(NMAX)) > 0) {
         const cudaError_t e = once_per_device(smem_attr, [] {
@@ -424,7 +430,7 @@ static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const flo
 template <int NMAX, bool EXACT>
 cudaError_t launch_poccd_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                            const float* seeds, float* theta, float* cost, float* ep, float* eo,
-                           int32_t* iters, uint32_t* trace, uint32_t* ready, cudaStream_t s) {
+                           int32_t* iters, TraceOut trace, uint32_t* ready, cudaStream_t s) {
     if (rb.pmask == 0u && rb.rx)
         return launch_poccd_r<NMAX, EXACT, 2>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
     if (rb.pmask == 0u)

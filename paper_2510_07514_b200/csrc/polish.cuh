@@ -235,7 +235,8 @@ __device__ __forceinline__ bool dogleg_direction(const DevRobotT<T>& rb, const D
 template <int NMAX, bool EXACT = false, class T>
 __device__ __forceinline__ bool single_coord_direction(const DevRobotT<T>& rb, const DevCfg& c,
                                                        const vec3<T> (&Jp)[NMAX], const vec3<T> (&Jo)[NMAX],
-                                                       const T (&W)[6], const T (&rho)[6], T (&dth)[NMAX]) {
+                                                       const T (&W)[6], const T (&rho)[6], T (&dth)[NMAX],
+                                                       int& ist_out) {
     const int n = rb.n;
     T wr[6];
 #pragma unroll
@@ -250,6 +251,7 @@ __device__ __forceinline__ bool single_coord_direction(const DevRobotT<T>& rb, c
             if (fabs(g) > gabs) { gabs = fabs(g); gbest = g; ist = j; }
         }
     }
+    ist_out = ist;
     if (gbest == T(0)) return false;
     const T Rt = T(c.R);
     const T step = (gbest > T(0)) ? -fmin(gabs, Rt) : fmin(gabs, Rt);

@@ -8,9 +8,12 @@
 //     converged seeds first, then cost, then slot) with a warp-shuffle +
 //     shared-memory reduction of 64-bit keys (tier | cost bits | slot).
 //   k_fk: batched FK + Jacobian (Eqs. 1, 7), one thread per configuration.
+//   k_pose_error64: fp64 pose error of given fp32 configurations (Eqs. 1, 4-5
+//     on the fp64 chain), one thread per configuration: success decided in
+//     fp64 from the returned theta, not from the solver's fp32 errors.
 #include <type_traits>
 
-#include "kin.cuh"
+#include "polish.cuh"
 
 namespace hjcd {
 
@@ -99,8 +102,9 @@ k_select_best(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCf
 }
 
 // REV: the chain specialisation of the stage kernels (kin.cuh fk), so this entry
-// point evaluates the same FK code path the solve does (K11 / K14)
-template <int NMAX, int REV>
+// point evaluates the same FK code path the solve does (K11 / K14); FAST: the
+// SFU-sincos variant of PO-CCD (K5), else the polish stage's exact sincos
+template <int NMAX, int REV, bool FAST>
 __global__ void __launch_bounds__(128)
 k_fk(const __grid_constant__ DevRobot rb, const float* __restrict__ q, int N, float* __restrict__ pose7,
      float* __restrict__ jac) {
@@ -112,7 +116,7 @@ k_fk(const __grid_constant__ DevRobot rb, const float* __restrict__ q, int N, fl
     for (int j = 0; j < NMAX; ++j) th[j] = (j < n) ? q[(long long)s * n + j] : 0.f;
     float3 P[NMAX], Z[NMAX], pe;
     Quat qe;
-    fk<NMAX, true, false, false, REV>(rb, th, P, Z, pe, qe);
+    fk<NMAX, true, false, FAST, REV>(rb, th, P, Z, pe, qe);
     float* o = pose7 + 7ll * s;
     o[0] = pe.x; o[1] = pe.y; o[2] = pe.z;
     o[3] = qe.w; o[4] = qe.x; o[5] = qe.y; o[6] = qe.z;
@@ -129,6 +133,32 @@ k_fk(const __grid_constant__ DevRobot rb, const float* __restrict__ q, int N, fl
             }
         }
     }
+}
+
+template <int NMAX>
+__global__ void __launch_bounds__(128)
+k_pose_error64(const __grid_constant__ DevRobotT<double> rb, const float* __restrict__ q,
+               const float* __restrict__ targets, int N, double* __restrict__ pos_err, double* __restrict__ ori_err) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= N) return;
+    const int n = rb.n;
+    double th[NMAX];
+#pragma unroll
+    for (int j = 0; j < NMAX; ++j) th[j] = (j < n) ? (double)q[(long long)s * n + j] : 0.0;
+    const TargetT<double> tg = load_target<double>(targets + 7ll * s);
+    const ResidT<double> r = eval_at<NMAX, false, 0>(rb, tg, th);
+    pos_err[s] = tg.valid ? r.ep : CUDART_INF;
+    ori_err[s] = tg.valid ? r.eo : CUDART_INF;
+}
+
+cudaError_t launch_pose_error64(const DevRobotT<double>& rb, const float* q, const float* targets, int N,
+                                double* pos_err, double* ori_err, cudaStream_t s) {
+    const int block = 128;
+    const int grid = (N + block - 1) / block;
+    if (rb.n <= 8) k_pose_error64<8><<<grid, block, 0, s>>>(rb, q, targets, N, pos_err, ori_err);
+    else if (rb.n <= 16) k_pose_error64<16><<<grid, block, 0, s>>>(rb, q, targets, N, pos_err, ori_err);
+    else k_pose_error64<32><<<grid, block, 0, s>>>(rb, q, targets, N, pos_err, ori_err);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_select_replicate(const DevRobot& rb, const DevCfg& c, const float* cost,
@@ -162,15 +192,22 @@ template cudaError_t launch_select_best<double>(const DevRobot&, const DevCfg&, 
                                                 const double*, const double*, double*, double*, double*, int32_t*,
                                                 cudaStream_t);
 
-cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, float* jac, cudaStream_t s) {
+cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, float* jac, cudaStream_t s,
+                      bool sfu) {
     const int block = 128;
     const int grid = (N + block - 1) / block;
     const int kind = rb.pmask ? 0 : (rb.rx ? 2 : 1);
     auto go = [&](auto nmax) {
         constexpr int NM = decltype(nmax)::value;
-        if (kind == 2) k_fk<NM, 2><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
-        else if (kind == 1) k_fk<NM, 1><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
-        else k_fk<NM, 0><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+        if (sfu) {
+            if (kind == 2) k_fk<NM, 2, true><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+            else if (kind == 1) k_fk<NM, 1, true><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+            else k_fk<NM, 0, true><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+            return;
+        }
+        if (kind == 2) k_fk<NM, 2, false><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+        else if (kind == 1) k_fk<NM, 1, false><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
+        else k_fk<NM, 0, false><<<grid, block, 0, s>>>(rb, q, N, pose7, jac);
     };
     if (rb.n <= 8) go(std::integral_constant<int, 8>());
     else if (rb.n <= 16) go(std::integral_constant<int, 16>());

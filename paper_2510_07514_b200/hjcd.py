@@ -26,8 +26,8 @@ EXPORTS = [
     "hjcd_robot_limits", "hjcd_config_default", "hjcd_workspace_size",
     "hjcd_workspace_size_host", "hjcd_solve", "hjcd_solve_timed", "hjcd_solve_host", "hjcd_ccd",
     "hjcd_solve_batch", "hjcd_select_topn", "hjcd_mmd", "hjcd_workspace_size_f64", "hjcd_solve_f64",
-    "hjcd_pjik_f64", "hjcd_fk", "hjcd_poccd", "hjcd_poccd_trace",
-    "hjcd_select_replicate", "hjcd_pjik", "hjcd_select_best", "hjcd_status_string",
+    "hjcd_pjik_f64", "hjcd_pose_error_f64", "hjcd_fk", "hjcd_fk_sfu", "hjcd_poccd", "hjcd_poccd_trace",
+    "hjcd_select_replicate", "hjcd_pjik", "hjcd_pjik_trace", "hjcd_select_best", "hjcd_status_string",
     "hjcd_last_cuda_error", "hjcd_version",
 ]
 
@@ -82,8 +82,10 @@ def lib():
         L.hjcd_solve_timed.argtypes = [P, P, P, i32, P, P, P, P, P, sz, P, P]
         L.hjcd_solve_host.argtypes = [P, P, P, i32, P, P, P, P, P, sz, P]
         L.hjcd_fk.argtypes = [P, P, i32, P, P, P]
+        L.hjcd_fk_sfu.argtypes = [P, P, i32, P, P, P]
+        L.hjcd_pose_error_f64.argtypes = [P, P, P, i32, P, P, P]
         L.hjcd_poccd.argtypes = [P, P, P, i32, P, P, P, P, P, P, P]
-        L.hjcd_poccd_trace.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P]
+        L.hjcd_poccd_trace.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P, P]
         L.hjcd_ccd.argtypes = [P, P, P, i32, P, P, P, P, P]
         L.hjcd_solve_batch.argtypes = [P, P, P, i32, i32, P, P, P, P, P, sz, P]
         L.hjcd_select_topn.argtypes = [P, P, P, i32, P, P, P, i32, P, P, P, P, P]
@@ -93,6 +95,7 @@ def lib():
         L.hjcd_pjik_f64.argtypes = [P, P, P, i32, P, P, P, P, P, P, P]
         L.hjcd_select_replicate.argtypes = [P, P, P, P, i32, P, P, P]
         L.hjcd_pjik.argtypes = [P, P, P, i32, P, P, P, P, P, P, P]
+        L.hjcd_pjik_trace.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P, P]
         L.hjcd_select_best.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P]
         L.hjcd_status_string.restype = C.c_char_p
         L.hjcd_last_cuda_error.restype = C.c_char_p
@@ -220,25 +223,45 @@ def workspace_size(robot: Robot, T: int, cfg: hjcd_config, host: bool = False) -
 
 
 class Workspace:
-    """Reusable device workspace (torch caching allocator owns the bytes)."""
+    """Reusable device workspace (torch caching allocator owns the bytes).
+    One solve at a time per workspace: the library refuses (HJCD_E_WORKSPACE)
+    a solve on another stream while the last one is in flight."""
 
     def __init__(self):
         self.buf = None
+        self.alloc_stream = None
 
-    def get(self, nbytes: int, device):
+    def get(self, nbytes: int, device, stream=None):
+        """The buffer (grown to nbytes), allocated on `stream` (torch stream) and,
+        when reused on another stream, recorded on it so the caching allocator
+        never hands the bytes out while that stream may still use them."""
         torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream(device)
         if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
-            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            with torch.cuda.stream(s):
+                self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+            self.alloc_stream = s
+        elif self.alloc_stream is None or self.alloc_stream.cuda_stream != s.cuda_stream:
+            self.buf.record_stream(s)
         return self.buf
 
 
+# the default workspaces: one per (device, stream), so solves on different
+# streams never share stage buffers
 _default_ws = {}
 
 
-def _ws_for(device, nbytes, ws: Optional[Workspace]):
+def _ws_for(device, nbytes, ws: Optional[Workspace], stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     if ws is None:
-        ws = _default_ws.setdefault(str(device), Workspace())
-    return ws.get(nbytes, device)
+        ws = _default_ws.setdefault((str(device), s.cuda_stream), Workspace())
+    return ws.get(nbytes, device, s)
+
+
+def _stream_of(stream, device):
+    torch = _torch()
+    return stream if stream is not None else torch.cuda.current_stream(device)
 
 
 # ---------------------------------------------------------------- API
@@ -254,13 +277,14 @@ def solve(robot: Robot, targets, cfg: Optional[hjcd_config] = None, out=None,
     _dev_f32(targets, (T, 7), "targets")
     dev = targets.device
     if out is None:
-        out = (torch.empty((T, robot.dof), dtype=torch.float32, device=dev),
-               torch.empty(T, dtype=torch.float32, device=dev),
-               torch.empty(T, dtype=torch.float32, device=dev),
-               torch.empty(T, dtype=torch.int32, device=dev))
+        with torch.cuda.stream(_stream_of(stream, dev)):   # results belong to the solve's stream
+            out = (torch.empty((T, robot.dof), dtype=torch.float32, device=dev),
+                   torch.empty(T, dtype=torch.float32, device=dev),
+                   torch.empty(T, dtype=torch.float32, device=dev),
+                   torch.empty(T, dtype=torch.int32, device=dev))
     q, pe, oe, st = out
     nbytes = workspace_size(robot, T, cfg)
-    ws = _ws_for(dev, nbytes, workspace)
+    ws = _ws_for(dev, nbytes, workspace, _stream_of(stream, dev))
     evp = None
     if events is not None:
         assert len(events) == 5
@@ -284,12 +308,13 @@ def solve_batch(robot: Robot, targets, N: int, cfg: Optional[hjcd_config] = None
     T = targets.shape[0]
     _dev_f32(targets, (T, 7), "targets")
     dev = targets.device
-    q = torch.empty((T, N, robot.dof), dtype=torch.float32, device=dev)
-    pe = torch.empty((T, N), dtype=torch.float32, device=dev)
-    oe = torch.empty((T, N), dtype=torch.float32, device=dev)
-    st = torch.empty(T, dtype=torch.int32, device=dev)
+    with torch.cuda.stream(_stream_of(stream, dev)):
+        q = torch.empty((T, N, robot.dof), dtype=torch.float32, device=dev)
+        pe = torch.empty((T, N), dtype=torch.float32, device=dev)
+        oe = torch.empty((T, N), dtype=torch.float32, device=dev)
+        st = torch.empty(T, dtype=torch.int32, device=dev)
     nbytes = workspace_size(robot, T, cfg)
-    ws = _ws_for(dev, nbytes, workspace)
+    ws = _ws_for(dev, nbytes, workspace, _stream_of(stream, dev))
     _check(lib().hjcd_solve_batch(robot.handle, C.byref(cfg), _ptr(targets), T, N, _ptr(q), _ptr(pe), _ptr(oe),
                                   _ptr(st), _ptr(ws), ws.numel(), _stream(stream)), "hjcd_solve_batch")
     return q, pe, oe, st
@@ -304,13 +329,14 @@ def solve_f64(robot: Robot, targets, cfg: Optional[hjcd_config] = None, workspac
     T = targets.shape[0]
     _dev_f32(targets, (T, 7), "targets")
     dev = targets.device
-    q = torch.empty((T, robot.dof), dtype=torch.float64, device=dev)
-    pe = torch.empty(T, dtype=torch.float64, device=dev)
-    oe = torch.empty(T, dtype=torch.float64, device=dev)
-    st = torch.empty(T, dtype=torch.int32, device=dev)
+    with torch.cuda.stream(_stream_of(stream, dev)):
+        q = torch.empty((T, robot.dof), dtype=torch.float64, device=dev)
+        pe = torch.empty(T, dtype=torch.float64, device=dev)
+        oe = torch.empty(T, dtype=torch.float64, device=dev)
+        st = torch.empty(T, dtype=torch.int32, device=dev)
     n = C.c_size_t()
     _check(lib().hjcd_workspace_size_f64(robot.handle, T, C.byref(cfg), C.byref(n)), "hjcd_workspace_size_f64")
-    ws = _ws_for(dev, n.value, workspace)
+    ws = _ws_for(dev, n.value, workspace, _stream_of(stream, dev))
     _check(lib().hjcd_solve_f64(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(q), _ptr(pe), _ptr(oe), _ptr(st),
                                 _ptr(ws), ws.numel(), _stream(stream)), "hjcd_solve_f64")
     return q, pe, oe, st
@@ -381,24 +407,44 @@ def solve_host(robot: Robot, targets_host, cfg: Optional[hjcd_config] = None, ou
         out = (torch.empty((T, robot.dof), dtype=torch.float32), torch.empty(T, dtype=torch.float32),
                torch.empty(T, dtype=torch.float32), torch.empty(T, dtype=torch.int32))
     q, pe, oe, st = out
-    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-    nbytes = workspace_size(robot, T, cfg, host=True)
-    ws = _ws_for(dev, nbytes, workspace)
-    _check(lib().hjcd_solve_host(robot.handle, C.byref(cfg), _ptr(tg), T, _ptr(q), _ptr(pe),
-                                 _ptr(oe), _ptr(st), _ptr(ws), ws.numel(), _stream(stream)),
-           "hjcd_solve_host")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    # the library launches on the CURRENT device: make it `dev` for the call,
+    # and default to that device's current stream
+    with torch.cuda.device(dev):
+        s = _stream_of(stream, dev)
+        nbytes = workspace_size(robot, T, cfg, host=True)
+        ws = _ws_for(dev, nbytes, workspace, s)
+        _check(lib().hjcd_solve_host(robot.handle, C.byref(cfg), _ptr(tg), T, _ptr(q), _ptr(pe),
+                                     _ptr(oe), _ptr(st), _ptr(ws), ws.numel(), s.cuda_stream),
+               "hjcd_solve_host")
     return q, pe, oe, st
 
 
-def fk(robot: Robot, q, jac: bool = False, stream=None):
-    """Eq. 1 / Eq. 7 on the GPU: q [N, dof] -> pose [N, 7] (and J [N, 6, dof])."""
+def fk(robot: Robot, q, jac: bool = False, stream=None, sfu: bool = False):
+    """Eq. 1 / Eq. 7 on the GPU: q [N, dof] -> pose [N, 7] (and J [N, 6, dof]).
+    sfu=True: the PO-CCD kernel's SFU-sincos FK (hjcd_fk_sfu)."""
     torch = _torch()
     N = q.shape[0]
     _dev_f32(q, (N, robot.dof), "q")
     pose = torch.empty((N, 7), dtype=torch.float32, device=q.device)
     J = torch.empty((N, 6, robot.dof), dtype=torch.float32, device=q.device) if jac else None
-    _check(lib().hjcd_fk(robot.handle, _ptr(q), N, _ptr(pose), _ptr(J), _stream(stream)), "hjcd_fk")
+    fn = lib().hjcd_fk_sfu if sfu else lib().hjcd_fk
+    _check(fn(robot.handle, _ptr(q), N, _ptr(pose), _ptr(J), _stream(stream)), "hjcd_fk")
     return (pose, J) if jac else pose
+
+
+def pose_error_f64(robot: Robot, q, targets, stream=None):
+    """fp64 pose errors of fp32 configurations q [N, dof] against targets [N, 7]
+    on the fp64 chain (hjcd_pose_error_f64) -> (pos_err [N], ori_err [N]) f64."""
+    torch = _torch()
+    N = q.shape[0]
+    _dev_f32(q, (N, robot.dof), "q")
+    _dev_f32(targets, (N, 7), "targets")
+    pe = torch.empty(N, dtype=torch.float64, device=q.device)
+    oe = torch.empty(N, dtype=torch.float64, device=q.device)
+    _check(lib().hjcd_pose_error_f64(robot.handle, _ptr(q), _ptr(targets), N, _ptr(pe), _ptr(oe), _stream(stream)),
+           "hjcd_pose_error_f64")
+    return pe, oe
 
 
 def poccd(robot: Robot, cfg: hjcd_config, targets, seeds=None, stream=None):
@@ -420,9 +466,11 @@ def poccd(robot: Robot, cfg: hjcd_config, targets, seeds=None, stream=None):
     return out
 
 
-def poccd_trace(robot: Robot, cfg: hjcd_config, targets, seeds=None, stream=None):
+def poccd_trace(robot: Robot, cfg: hjcd_config, targets, seeds=None, stream=None, history: bool = False):
     """hjcd_poccd that also returns every seed's decision words:
-    trace [T, M, ccd_iters] uint32 (as int32), unwritten past iters = 0."""
+    trace [T, M, ccd_iters] uint32 (as int32), unwritten past iters = 0, and
+    with history=True theta_hist [T, M, ccd_iters + 1, n] (theta at the start
+    of every iteration, NaN past iters)."""
     torch = _torch()
     T, n, M = targets.shape[0], robot.dof, cfg.M
     _dev_f32(targets, (T, 7), "targets")
@@ -435,9 +483,12 @@ def poccd_trace(robot: Robot, cfg: hjcd_config, targets, seeds=None, stream=None
                eo=torch.empty((T, M), dtype=torch.float32, device=d),
                iters=torch.empty((T, M), dtype=torch.int32, device=d),
                trace=torch.zeros((T, M, max(cfg.ccd_iters, 1)), dtype=torch.int32, device=d))
+    if history:
+        out["theta_hist"] = torch.full((T, M, cfg.ccd_iters + 1, n), float("nan"), dtype=torch.float32, device=d)
     _check(lib().hjcd_poccd_trace(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(seeds),
                                   _ptr(out["theta"]), _ptr(out["cost"]), _ptr(out["ep"]), _ptr(out["eo"]),
-                                  _ptr(out["iters"]), _ptr(out["trace"]), _stream(stream)), "hjcd_poccd_trace")
+                                  _ptr(out["iters"]), _ptr(out["trace"]), _ptr(out.get("theta_hist")),
+                                  _stream(stream)), "hjcd_poccd_trace")
     return out
 
 
@@ -488,6 +539,31 @@ def pjik(robot: Robot, cfg: hjcd_config, targets, seeds, stream=None):
     _check(lib().hjcd_pjik(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(seeds),
                            _ptr(out["theta"]), _ptr(out["ep"]), _ptr(out["eo"]),
                            _ptr(out["counts"]), _ptr(out["iters"]), _stream(stream)), "hjcd_pjik")
+    return out
+
+
+def pjik_trace(robot: Robot, cfg: hjcd_config, targets, seeds, stream=None, history: bool = False):
+    """hjcd_pjik that also returns every seed's decision words:
+    trace [T, B, lm_iters] uint32 (as int32), zero where no step was taken, and
+    with history=True theta_hist [T, B, lm_iters + 1, n] (theta at the start
+    of every iteration, NaN past iters)."""
+    torch = _torch()
+    T, n = targets.shape[0], robot.dof
+    _dev_f32(targets, (T, 7), "targets")
+    _dev_f32(seeds, (T, cfg.B, n), "seeds")
+    d = targets.device
+    out = dict(theta=torch.empty((T, cfg.B, n), dtype=torch.float32, device=d),
+               ep=torch.empty((T, cfg.B), dtype=torch.float32, device=d),
+               eo=torch.empty((T, cfg.B), dtype=torch.float32, device=d),
+               counts=torch.empty((T, cfg.B, 4), dtype=torch.int32, device=d),
+               iters=torch.empty((T, cfg.B), dtype=torch.int32, device=d),
+               trace=torch.zeros((T, cfg.B, max(cfg.lm_iters, 1)), dtype=torch.int32, device=d))
+    if history:
+        out["theta_hist"] = torch.full((T, cfg.B, cfg.lm_iters + 1, n), float("nan"), dtype=torch.float32, device=d)
+    _check(lib().hjcd_pjik_trace(robot.handle, C.byref(cfg), _ptr(targets), T, _ptr(seeds),
+                                 _ptr(out["theta"]), _ptr(out["ep"]), _ptr(out["eo"]), _ptr(out["counts"]),
+                                 _ptr(out["iters"]), _ptr(out["trace"]), _ptr(out.get("theta_hist")),
+                                 _stream(stream)), "hjcd_pjik_trace")
     return out
 
 

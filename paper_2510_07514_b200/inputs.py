@@ -108,15 +108,20 @@ def planar(links: Sequence[float], lo: float = -math.pi, hi: float = math.pi) ->
 
 def extend(chain: Chain, target_dof: int) -> Chain:
     """Cyclic replication of the DoF joints (origin, axis, limits) before the
-    end effector (R34; SPEC extend_dof)."""
+    end effector (R34; SPEC extend_dof).  A trailing run of FIXED
+    joints belongs to the end-effector offset, so the replicas go before it."""
     if target_dof < chain.dof:
         raise ValueError("target_dof < dof")
     base = [j for j in chain.joints if j.type != FIXED]
-    joints = list(chain.joints)
+    tail = len(chain.joints)
+    while tail > 0 and chain.joints[tail - 1].type == FIXED:
+        tail -= 1
+    joints = list(chain.joints[:tail])
     i = 0
     while sum(1 for j in joints if j.type != FIXED) < target_dof:
         joints.append(base[i % len(base)])
         i += 1
+    joints += chain.joints[tail:]
     return Chain(f"{chain.name}_x{target_dof}", joints, chain.ee_xyz, chain.ee_quat)
 
 

@@ -95,7 +95,7 @@ def test_config_and_workspace_validation(hjcd_lib):
     fake = C.c_void_p(256)
     assert L.hjcd_solve(r.handle, C.byref(c), fake, 10, fake, fake, fake, fake, fake, 1024, None) == 4
     assert L.hjcd_solve(r.handle, C.byref(c), fake, 0, fake, fake, fake, fake, fake, 1 << 40, None) == 1
-    assert L.hjcd_status_string(4) == b"workspace too small or misaligned"
+    assert L.hjcd_status_string(4) == b"workspace too small, misaligned, or in use on another stream"
 
 
 def test_oracle_and_cuda_path_share_nothing():
@@ -141,9 +141,11 @@ def test_new_entry_points_validate_before_cuda(hjcd_lib):
     big = hjcd_lib.default_config(M=3000)
     assert L.hjcd_poccd(r.handle, C.byref(big), fake, 1, None, fake, fake, None, None, None, None) == 2
     assert L.hjcd_poccd_trace(r.handle, C.byref(big), fake, 1, None, fake, fake, None, None, None, fake,
-                              None) == 2
+                              None, None) == 2
     # the decision trace needs its buffer
     assert L.hjcd_poccd_trace(r.handle, C.byref(c), fake, 1, None, fake, fake, None, None, None, None,
-                              None) == 1
+                              None, None) == 1
+    assert L.hjcd_pjik_trace(r.handle, C.byref(c), fake, 1, fake, fake, fake, fake, None, None, None,
+                             None, None) == 1
     ok = hjcd_lib.default_config(M=3000, ccd_early_exit=0)
     assert L.hjcd_workspace_size(r.handle, 10, C.byref(ok), C.byref(n32)) == 0

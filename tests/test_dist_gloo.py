@@ -82,3 +82,36 @@ def test_sharded_equals_single_process(T):
     ref = oracle.solve(ch, dict(P), tg)
     assert np.array_equal(got[0], ref[0].astype(np.float32))
     assert np.array_equal(got[3], ref[3])
+
+
+def _bench(args, env_extra):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py")] + args, cwd=root, env=env,
+                       capture_output=True, text=True, timeout=600)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    return r.returncode, (json.loads(lines[-1]) if lines else None), r.stderr
+
+
+def test_bench_gpus_flag_launches_ranks():
+    # bench.py --gpus 2 outside torchrun re-launches itself under
+    # torch.distributed.run with 2 ranks (127.0.0.1 rendezvous); --check-launch
+    # runs the multi-rank plumbing without a solve, so it is CPU-testable (gloo)
+    env = {"HJCD_DIST_BACKEND": "gloo"}
+    env_clean = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    os_env = os.environ.copy()
+    try:
+        os.environ.clear()
+        os.environ.update(env_clean)
+        rc, out, err = _bench(["--gpus", "2", "--check-launch"], env)
+        assert rc == 0, err[-2000:]
+        assert out == {"check": "launch", "n_gpus": 2, "ranks": [0, 1], "backend": "gloo"}
+        # under a launcher the world size must equal --gpus
+        rc, out, err = _bench(["--gpus", "2", "--check-launch"], {"WORLD_SIZE": "1"})
+        assert rc == 2 and "WORLD_SIZE=1 but --gpus 2" in err
+    finally:
+        os.environ.clear()
+        os.environ.update(os_env)
