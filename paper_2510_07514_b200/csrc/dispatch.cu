@@ -2,6 +2,8 @@
 // kernels (no per-joint guards) for the benchmarked chains n = 7, 8, 14 and
 // the paper's Table II DoFs 12, 18, 24, and NMAX-bounded kernels (uniform
 // `j < n` guards) for every other n <= 32.
+#include <cstdlib>
+
 #include "hjcd_internal.h"
 
 namespace hjcd {
@@ -13,9 +15,32 @@ int poccd_nmax(int n) {   // must match launch_poccd's choice below
     }
 }
 
+// K17: the two-seeds-per-thread packed kernel for the stop-rule launch with
+// fused seeds at n <= 8 (HJCD_POCCD_X2=0 in the environment selects the
+// one-seed-per-thread kernel, for A/B measurements)
+static bool use_x2(int n) {
+    static const int env = [] {
+        const char* e = std::getenv("HJCD_POCCD_X2");
+        return e ? std::atoi(e) : 1;
+    }();
+    return env != 0 && n <= 8;
+}
+
+int poccd_cluster_ctas(int M, int n) {
+    int nt, CL;
+    if (use_x2(n)) texit_shape_x2(M, nt, CL);
+    else texit_shape(M, poccd_nmax(n), nt, CL);
+    return CL;
+}
+
 cudaError_t launch_poccd(const DevRobot& rb, const DevCfg& c, const float* targets, int T,
                          const float* seeds, float* theta, float* cost, float* ep, float* eo,
                          int32_t* iters, cudaStream_t s, TraceOut trace, uint32_t* ready) {
+    if (c.ccd_early_exit && !seeds && use_x2(rb.n)) {
+        if (rb.n == 7) return launch_poccd_x2_t<7, true>(rb, c, targets, T, theta, cost, ep, eo, iters, trace, ready, s);
+        if (rb.n == 8) return launch_poccd_x2_t<8, true>(rb, c, targets, T, theta, cost, ep, eo, iters, trace, ready, s);
+        return launch_poccd_x2_t<8, false>(rb, c, targets, T, theta, cost, ep, eo, iters, trace, ready, s);
+    }
     switch (rb.n) {   // exact instantiations for the benchmarked chains, bounded ones otherwise
         case 7: return launch_poccd_t<7, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);
         case 8: return launch_poccd_t<8, true>(rb, c, targets, T, seeds, theta, cost, ep, eo, iters, trace, ready, s);

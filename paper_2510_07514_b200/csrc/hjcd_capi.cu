@@ -340,9 +340,7 @@ cudaError_t solve_linked(const hjcd_robot* r, const DevCfg& d, const float* targ
     link.ready = (uint32_t*)(ws + L.ready);
     link.cost = cost1;
     link.theta = theta1;
-    int nt, CL;
-    texit_shape(d.M, poccd_nmax(r->dof), nt, CL);
-    link.need = (uint32_t)CL;
+    link.need = (uint32_t)poccd_cluster_ctas(d.M, r->dof);
     link.spin_limit = (1ull << 26) * (unsigned long long)(1 + d.ccd_iters / 64);
     link.Mpad = 2;
     while (link.Mpad < d.M) link.Mpad <<= 1;

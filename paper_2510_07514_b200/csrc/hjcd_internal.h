@@ -94,6 +94,13 @@ inline void texit_shape(int M, int nmax, int& nt, int& CL) {
     CL = (M + nt - 1) / nt;
 }
 
+// the packed two-seeds-per-thread launch (K17): threads per CTA and CTAs per cluster
+inline void texit_shape_x2(int M, int& nt, int& CL) {
+    const int pairs = (M + 1) / 2;
+    nt = pairs < 128 ? (pairs + 31) / 32 * 32 : 128;
+    CL = (pairs + nt - 1) / nt;
+}
+
 #ifdef HJCD_PROBE
 // A/B diagnostic build only: %globaltimer stamps of the K10 schedule, stored
 // after the readiness counts: [5][T] = PO-CCD first CTA start, last CTA end,
@@ -140,8 +147,16 @@ cudaError_t launch_coop_t(const DevRobotT<T>& rb, const DevCfg& c, const float* 
                           const float* seeds, T* theta, T* ep, T* eo, int32_t* counts, int32_t* iters,
                           cudaStream_t s, const StageLink& link);
 
+template <int NMAX, bool EXACT>
+cudaError_t launch_poccd_x2_t(const DevRobot& rb, const DevCfg& c, const float* targets, int T, float* theta,
+                              float* cost, float* ep, float* eo, int32_t* iters, TraceOut trace, uint32_t* ready,
+                              cudaStream_t s);
+
 // the joint bound NMAX of the PO-CCD kernel launch_poccd picks for n DoF (dispatch.cu)
 int poccd_nmax(int n);
+// CTAs per target cluster of launch_poccd's stop-rule launch (M seeds, n DoF,
+// fused Philox seeds): the readiness count the dependent PJ-IK waits for (K10)
+int poccd_cluster_ctas(int M, int n);
 
 // launchers (dispatch.cu, select.cu); all asynchronous on `s`
 cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, float* jac,
