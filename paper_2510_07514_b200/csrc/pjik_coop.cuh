@@ -31,8 +31,7 @@ struct CoopSmem {
     T* c0;         // [nt]
     T* n0;         // [nt]
     int* flags;    // [nt]  bit0 LM, bit1 dogleg, bit2 single
-    unsigned char* own;    // [64 nt]  pending item -> owner slot
-    unsigned char* ownq;   // [64 nt]  pending item -> index in the owner's cascade
+    unsigned char* own;    // [nt]  rank among the failing seeds -> owner slot
     unsigned long long* ok;   // [nt]  success bits in cascade order
 };
 
@@ -49,13 +48,12 @@ __device__ __forceinline__ CoopSmem<T> coop_smem(void* base, int nt) {
     s.n0 = f; f += nt;
     s.flags = (int*)f;
     s.own = (unsigned char*)(s.flags + nt);
-    s.ownq = s.own + 64 * nt;
     return s;
 }
 
 template <class T, int NMAX>
 size_t coop_smem_bytes(int nt) {
-    return (size_t)nt * (8 + sizeof(T) * (4 * NMAX + 6 + 2) + 4 + 2 * 64);
+    return (size_t)nt * (8 + sizeof(T) * (4 * NMAX + 6 + 2) + 4 + 1);
 }
 
 // REV: every DoF joint is revolute (no per-joint type branches)
@@ -66,7 +64,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
             T* __restrict__ theta_out, T* __restrict__ ep_out, T* __restrict__ eo_out,
             int32_t* __restrict__ counts_out, int32_t* __restrict__ iters_out, const StageLink link) {
     extern __shared__ unsigned long long coop_raw[];
-    __shared__ int s_wtot[8];   // per-warp item totals (<= 256 threads)
+    __shared__ int s_wtot[8];   // per-warp counts of failing seeds (<= 256 threads)
     __shared__ T s_alpha[32];   // line-search steps beta^-a, a = 0..A (A <= 31), by repeated products
     const int nt = blockDim.x;
     const CoopSmem<T> S = coop_smem<T, NMAX>(coop_raw, nt);
@@ -175,7 +173,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
         if (k == c.lm_iters) break;
 
         bool need = false, have_lm = false, accepted = false;
-        int flags = 0, items = 0, ist = 0;
+        int flags = 0, ist = 0;
         uint32_t word = 0u;   // hjcd_pjik_trace decision word of this iteration
         T W[6], c0 = T(0);
         if (live) {
@@ -248,39 +246,30 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                     S.c0[b] = c0;
                     S.n0[b] = n0;
                     S.flags[b] = flags;
-                    items = ((flags & 1) ? c.A : 0) + ((flags & 2) ? 1 : 0) + ((flags & 4) ? c.A + 1 : 0);
                 }
-                int incl = items;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int v = __shfl_up_sync(0xffffffffu, incl, off);
-                    if (lane >= off) incl += v;
-                }
-                if (lane == 31) s_wtot[b >> 5] = incl;
+                // the failing seeds' cascades as fixed-width item ranges:
+                // item (rank, q) = cascade position q < Q = 2A + 2 (LM
+                // alpha_1..alpha_A, dogleg, single alpha_0..alpha_A) of the
+                // rank-th failing seed; a direction that did not form leaves
+                // holes, skipped by the evaluating lane
+                const unsigned fail = __ballot_sync(0xffffffffu, need);
+                int rank = __popc(fail & ((1u << lane) - 1u));
+                if (lane == 0) s_wtot[b >> 5] = __popc(fail);
                 S.ok[b] = 0ull;
                 __syncthreads();
                 P2MARK(3);
+                int nfail = 0;
                 for (int w = 0; w < (nt >> 5); ++w) {
                     const int v = s_wtot[w];
-                    if (w < (b >> 5)) incl += v;
-                    total += v;
+                    if (w < (b >> 5)) rank += v;
+                    nfail += v;
                 }
+                total = nfail * (2 * c.A + 2);
 #ifdef HJCD_PROBE2
                 p2_items += total;
 #endif
-                if (total == 0) {   // uniform over the CTA: no trial pending anywhere
-                    if (need) {     // every direction failed to form: Alg. 4 l.17 (R25)
-                        perturb<NMAX, EXACT, true>(rb, c, th, T(c.sigma_lm), tid, (uint32_t)b, P_PJPERT, (uint32_t)k);
-                        cnt[3]++;
-                        word = 3u | (1u << 15);
-                    }
-                    break;
-                }
-                // item -> (owner, index) table: each failing seed fills its range
-                for (int i = 0; i < items; ++i) {
-                    S.own[incl - items + i] = (unsigned char)b;
-                    S.ownq[incl - items + i] = (unsigned char)i;
-                }
+                if (total == 0) break;   // uniform over the CTA: no seed failed its alpha = 1 trial
+                if (need) S.own[rank] = (unsigned char)b;
                 __syncthreads();
                 P2MARK(4);
             }
@@ -295,9 +284,11 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                         x[j] = (EXACT || j < n) ? clampf(th[j] + dth[j], rb.j[j].lo, rb.j[j].hi) : T(0);
                 } else {
                     if (it >= total) break;
-                    o = S.own[it];
-                    qq = S.ownq[it];   // item index within the owner's list
-                    decode_item(qq, S.flags[o], c.A, kind, a);
+                    const int rk = it / (2 * c.A + 2);
+                    qq = it - rk * (2 * c.A + 2);   // cascade position in the owner's list
+                    o = S.own[rk];
+                    decode_item(qq, c.A, kind, a);
+                    if (!((S.flags[o] >> kind) & 1)) continue;   // that direction did not form
                     const T alpha = s_alpha[a];
 #pragma unroll
                     for (int j = 0; j < NMAX; ++j)
@@ -350,7 +341,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                 if (m) {
                     const int qq = __ffsll((long long)m) - 1;   // first success in cascade order
                     int kind, a;
-                    decode_item(qq, flags, c.A, kind, a);
+                    decode_item(qq, c.A, kind, a);
                     const T alpha = s_alpha[a];
 #pragma unroll
                     for (int j = 0; j < NMAX; ++j)

@@ -260,15 +260,15 @@ __device__ __forceinline__ bool single_coord_direction(const DevRobotT<T>& rb, c
     return true;
 }
 
-// cascade item q of a seed with flags f -> (direction kind, alpha index)
-__device__ __forceinline__ void decode_item(int q, int f, int A, int& kind, int& a) {
-    const int nlm = (f & 1) ? A : 0;
-    const int ndl = (f & 2) ? 1 : 0;
-    if (q < nlm) { kind = 0; a = q + 1; return; }
-    q -= nlm;
-    if (q < ndl) { kind = 1; a = 0; return; }
+// cascade position q < 2A + 2 of a seed -> (direction kind, alpha index):
+// LM alpha_1..alpha_A, dogleg, single coordinate alpha_0..alpha_A (Alg. 4
+// order, R22-R24); the lowest successful position is the step the sequential
+// cascade takes
+__device__ __forceinline__ void decode_item(int q, int A, int& kind, int& a) {
+    if (q < A) { kind = 0; a = q + 1; return; }
+    if (q == A) { kind = 1; a = 0; return; }
     kind = 2;
-    a = q - ndl;
+    a = q - A - 1;
 }
 
 }  // namespace hjcd
