@@ -439,15 +439,16 @@ def main():
     pjik_flops = pj_iters_sum * flops_pjik_iter(n)
     ach = poccd_flops / (kmean["k_poccd"] / 1e3) / 1e12
     traffic, exec_flops = None, None
+    kname = hjcd.poccd_kernel(robot, cfg)   # k_poccd_x2 (K17) or k_poccd
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
         if T_local == CONFIGS[args.config][1]:   # the captured launch size only
-            traffic = tj.get(args.config, {}).get("k_poccd")
-            exec_flops = tj.get("_executed_fp32_flops", {}).get(args.config, {}).get("k_poccd")
+            traffic = tj.get(args.config, {}).get(kname)
+            exec_flops = tj.get("_executed_fp32_flops", {}).get(args.config, {}).get(kname)
     except Exception:
         pass
-    roofline = {"bound": "alu", "kernel": "k_poccd", "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
+    roofline = {"bound": "alu", "kernel": kname, "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": ach / peak_tf, "traffic": traffic,
                 "peak_source": f"148 SM x 128 FP32 lanes x 2 x {mhz:.0f} MHz ({peak_src})",
                 "algorithmic_flops_per_launch": poccd_flops,

@@ -340,6 +340,11 @@ hjcd_status hjcd_mmd(const float* X, int32_t N, const float* Y, int32_t N2, int3
                      float* mmd2, float* bandwidth, hjcd_stream_t stream);
 
 const char* hjcd_status_string(hjcd_status s);
+
+/* The name of the PO-CCD kernel hjcd_solve launches for this robot and config
+ * ("k_poccd_x2": two seeds per thread, packed fp32, K17; "k_poccd"
+ * otherwise), for profilers and roofline reports.  Static storage; "" on NULL. */
+const char* hjcd_poccd_kernel(const hjcd_robot* r, const hjcd_config* c);
 /* text of the last CUDA error seen by this thread's calls ("" if none) */
 const char* hjcd_last_cuda_error(void);
 /* library / build identification, e.g. "hjcd 0.1 sm_100a" */

@@ -26,6 +26,8 @@ static bool use_x2(int n) {
     return env != 0 && n <= 8;
 }
 
+bool poccd_uses_x2(int n, bool ccd_early_exit) { return ccd_early_exit && use_x2(n); }
+
 int poccd_cluster_ctas(int M, int n) {
     int nt, CL;
     if (use_x2(n)) texit_shape_x2(M, nt, CL);

@@ -783,6 +783,11 @@ const char* hjcd_status_string(hjcd_status s) {
     return "unknown status";
 }
 
+const char* hjcd_poccd_kernel(const hjcd_robot* r, const hjcd_config* c) {
+    if (!r || !c) return "";
+    return poccd_uses_x2(r->dof, c->ccd_early_exit != 0) ? "k_poccd_x2" : "k_poccd";
+}
+
 const char* hjcd_last_cuda_error(void) { return g_cuda_err.c_str(); }
 
 const char* hjcd_version(void) { return "hjcd 0.1 sm_100a"; }

@@ -157,6 +157,8 @@ int poccd_nmax(int n);
 // CTAs per target cluster of launch_poccd's stop-rule launch (M seeds, n DoF,
 // fused Philox seeds): the readiness count the dependent PJ-IK waits for (K10)
 int poccd_cluster_ctas(int M, int n);
+// true if hjcd_solve's PO-CCD stage runs k_poccd_x2 (K17) for n DoF
+bool poccd_uses_x2(int n, bool ccd_early_exit);
 
 // launchers (dispatch.cu, select.cu); all asynchronous on `s`
 cudaError_t launch_fk(const DevRobot& rb, const float* q, int N, float* pose7, float* jac,

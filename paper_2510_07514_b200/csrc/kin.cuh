@@ -148,8 +148,8 @@ __device__ __forceinline__ void sincos_b(double x, double* s, double* c) { sinco
 // every column update a*col + b*col' is one FMUL2 + one FFMA2 for rows 0-1
 // plus the scalar row 2: 22 instead of 33 issue slots per joint.  Same
 // operations per element as the scalar form below; outputs unpacked for free.
-template <int NMAX, bool FRAMES, bool EXACT, bool FAST>
-__device__ __forceinline__ void fk_rx2(const DevRobotT<float>& rb, const float (&th)[NMAX], float3 (&P)[NMAX],
+template <int NMAX, bool FRAMES, bool EXACT, bool FAST, class A>
+__device__ __forceinline__ void fk_rx2(const DevRobotT<float>& rb, const A& th, float3 (&P)[NMAX],
                                        float3 (&Z)[NMAX], float3& pe, Quat& qe) {
     f2 C0 = mk2(1.f, 0.f), C1 = mk2(0.f, 1.f), C2 = mk2(0.f, 0.f);   // R[0,3], R[1,4], R[2,5]
     float r6 = 0.f, r7 = 0.f, r8 = 1.f;                              // R[6], R[7], R[8]
@@ -214,8 +214,10 @@ __device__ __forceinline__ void fk_rx2(const DevRobotT<float>& rb, const float (
 // every F_j rotation is Rx(alpha_j) (rb.rx, DESIGN K11): the rotation product
 // skips the structural zeros (12 instead of 27 multiply-adds per joint) with
 // the same operation order on the non-zero terms, i.e. the same bits.
-template <int NMAX, bool FRAMES, bool EXACT = false, bool FAST = false, int REV = 0, class T>
-__device__ __forceinline__ void fk(const DevRobotT<T>& rb, const T (&th)[NMAX], vec3<T> (&P)[NMAX],
+// th: a T[NMAX] array, or any type whose th[j] yields joint j's value (a trial
+// point computed joint by joint, polish.cuh TrialTheta)
+template <int NMAX, bool FRAMES, bool EXACT = false, bool FAST = false, int REV = 0, class T, class A>
+__device__ __forceinline__ void fk(const DevRobotT<T>& rb, const A& th, vec3<T> (&P)[NMAX],
                                    vec3<T> (&Z)[NMAX], vec3<T>& pe, QuatT<T>& qe) {
     if constexpr (REV == 2 && sizeof(T) == 4 && NMAX <= 8) {   // (more spills above 8 DoF)
 #ifndef HJCD_NO_K14

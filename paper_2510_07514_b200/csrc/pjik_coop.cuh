@@ -68,6 +68,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
     __shared__ T s_alpha[32];   // line-search steps beta^-a, a = 0..A (A <= 31), by repeated products
     const int nt = blockDim.x;
     const CoopSmem<T> S = coop_smem<T, NMAX>(coop_raw, nt);
+    constexpr bool SPEC_DIRS = NMAX >= 16 && sizeof(T) == 4;   // K19
     const int n = rb.n;
     const int used = c.copies * c.K;
     const int t = blockIdx.x;
@@ -198,14 +199,43 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                     if (EXACT || j < n) {
                         rn[0] += Jp[j].x * Jp[j].x; rn[1] += Jp[j].y * Jp[j].y; rn[2] += Jp[j].z * Jp[j].z;
                         rn[3] += Jo[j].x * Jo[j].x; rn[4] += Jo[j].y * Jo[j].y; rn[5] += Jo[j].z * Jo[j].z;
-                        invD[j] = rcp_nr(fmax(dot3(Jp[j], Jp[j]) + dot3(Jo[j], Jo[j]), T(c.d_floor)));
+                        if constexpr (!SPEC_DIRS)
+                            invD[j] = rcp_nr(fmax(dot3(Jp[j], Jp[j]) + dot3(Jo[j], Jo[j]), T(c.d_floor)));
                     }
                 }
 #pragma unroll
                 for (int i = 0; i < 6; ++i) W[i] = T(i < 3 ? c.w_p : c.w_o) * rcp_nr(T(1) + sqrt(rn[i]));
             }
             c0 = cost_w(W, r.rho);
-            have_lm = lm_direction<NMAX, EXACT>(rb, c, Jp, Jo, invD, W, r.rho, dth);
+            have_lm = lm_direction<NMAX, EXACT, SPEC_DIRS>(rb, c, Jp, Jo, invD, W, r.rho, dth);
+            // theta and the LM direction into this seed's record: the alpha = 1
+            // trial reads them from there (K19), and so does the cooperative
+            // cascade if that trial fails
+#pragma unroll
+            for (int j = 0; j < NMAX; ++j) {
+                S.th[j * nt + b] = th[j];
+                S.dir[(0 * NMAX + j) * nt + b] = dth[j];
+            }
+            if constexpr (SPEC_DIRS) {
+                // K19, high DoF: the fallback directions now, while the
+                // Jacobian is live, so that it is dead during the trials (6n
+                // registers: no spills at 18 / 24 DoF); seeds whose alpha = 1
+                // trial then succeeds did this work in vain
+                flags = have_lm ? 1 : 0;
+                if (dogleg_direction<NMAX, EXACT>(rb, c, Jp, Jo, r.rho, dth, tt)) {   // Eqs. 14-15
+                    flags |= 2;
+#pragma unroll
+                    for (int j = 0; j < NMAX; ++j) S.dir[(1 * NMAX + j) * nt + b] = dth[j];
+                }
+                if (single_coord_direction<NMAX, EXACT>(rb, c, Jp, Jo, W, r.rho, dth, ist)) {   // Eq. 16
+                    flags |= 4;
+#pragma unroll
+                    for (int j = 0; j < NMAX; ++j) S.dir[(2 * NMAX + j) * nt + b] = dth[j];
+                }
+                // theta back from its record: not held in registers across the directions
+#pragma unroll
+                for (int j = 0; j < NMAX; ++j) th[j] = S.th[j * nt + b];
+            }
         }
         P2MARK(1);
 
@@ -225,21 +255,18 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                     T n0 = T(0);
 #pragma unroll
                     for (int i = 0; i < 6; ++i) n0 += r.rho[i] * r.rho[i];
-                    flags = have_lm ? 1 : 0;
+                    if constexpr (!SPEC_DIRS) {
+                        flags = have_lm ? 1 : 0;   // theta and the LM direction are published already
+                        if (dogleg_direction<NMAX, EXACT>(rb, c, Jp, Jo, r.rho, dth, tt)) {   // Eqs. 14-15
+                            flags |= 2;
 #pragma unroll
-                    for (int j = 0; j < NMAX; ++j) {
-                        S.th[j * nt + b] = th[j];
-                        S.dir[(0 * NMAX + j) * nt + b] = dth[j];
-                    }
-                    if (dogleg_direction<NMAX, EXACT>(rb, c, Jp, Jo, r.rho, dth, tt)) {   // Eqs. 14-15
-                        flags |= 2;
+                            for (int j = 0; j < NMAX; ++j) S.dir[(1 * NMAX + j) * nt + b] = dth[j];
+                        }
+                        if (single_coord_direction<NMAX, EXACT>(rb, c, Jp, Jo, W, r.rho, dth, ist)) {   // Eq. 16
+                            flags |= 4;
 #pragma unroll
-                        for (int j = 0; j < NMAX; ++j) S.dir[(1 * NMAX + j) * nt + b] = dth[j];
-                    }
-                    if (single_coord_direction<NMAX, EXACT>(rb, c, Jp, Jo, W, r.rho, dth, ist)) {   // Eq. 16
-                        flags |= 4;
-#pragma unroll
-                        for (int j = 0; j < NMAX; ++j) S.dir[(2 * NMAX + j) * nt + b] = dth[j];
+                            for (int j = 0; j < NMAX; ++j) S.dir[(2 * NMAX + j) * nt + b] = dth[j];
+                        }
                     }
 #pragma unroll
                     for (int i = 0; i < 6; ++i) S.W[i * nt + b] = W[i];
@@ -276,12 +303,8 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
             bool own_ok = false;
             for (int it = b;; it += nt) {
                 int o = b, qq = 0, kind = 0, a = 0;
-                T x[NMAX];
                 if (phase == 0) {
                     if (it != b || !pending) break;
-#pragma unroll
-                    for (int j = 0; j < NMAX; ++j)
-                        x[j] = (EXACT || j < n) ? clampf(th[j] + dth[j], rb.j[j].lo, rb.j[j].hi) : T(0);
                 } else {
                     if (it >= total) break;
                     const int rk = it / (2 * c.A + 2);
@@ -289,14 +312,9 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                     o = S.own[rk];
                     decode_item(qq, c.A, kind, a);
                     if (!((S.flags[o] >> kind) & 1)) continue;   // that direction did not form
-                    const T alpha = s_alpha[a];
-#pragma unroll
-                    for (int j = 0; j < NMAX; ++j)
-                        x[j] = (EXACT || j < n)
-                                   ? clampf(S.th[j * nt + o] + alpha * S.dir[(kind * NMAX + j) * nt + o], rb.j[j].lo,
-                                            rb.j[j].hi)
-                                   : T(0);
                 }
+                // clamp(theta + alpha d), joint by joint (alpha = 1 in phase 0: th + 1 * d = th + d exactly)
+                const TrialTheta<T> x{rb, S.th + o, S.dir + (kind * NMAX) * nt + o, nt, s_alpha[a]};
                 const ResidT<T> rt = eval_at<NMAX, EXACT, REV>(rb, tg, x);
                 bool ok;
                 if (kind == 1) {   // dogleg: unweighted |rho| (R23)
@@ -315,22 +333,21 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                 }
                 if (phase == 0) {
                     own_ok = ok;
-                    if (ok) {   // the LM step at alpha = 1 is accepted
-#pragma unroll
-                        for (int j = 0; j < NMAX; ++j) tt[j] = x[j];
-                    }
                 } else if (ok) {
                     atomicOr(&S.ok[o], 1ull << qq);
                 }
             }
             if (phase == 0) {
                 P2MARK(2);
-                if (own_ok) {
+                if (own_ok) {   // the LM step at alpha = 1 is accepted: the trial point
                     accepted = true;
                     cnt[0]++;
                     word = 1u << 15;   // LM step, alpha index 0
 #pragma unroll
-                    for (int j = 0; j < NMAX; ++j) th[j] = tt[j];
+                    for (int j = 0; j < NMAX; ++j)
+                        if (EXACT || j < n)
+                            th[j] = clampf(th[j] + (SPEC_DIRS ? S.dir[(0 * NMAX + j) * nt + b] : dth[j]), rb.j[j].lo,
+                                           rb.j[j].hi);
                 }
                 continue;
             }

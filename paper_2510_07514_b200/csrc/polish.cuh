@@ -90,8 +90,23 @@ __device__ __forceinline__ T cost_w(const T (&W)[6], const T (&rho)[6]) {
     return T(0.5) * s;
 }
 
-template <int NMAX, bool EXACT = false, int REV = 0, class T>
-__device__ __forceinline__ ResidT<T> eval_at(const DevRobotT<T>& rb, const TargetT<T>& tg, const T (&th)[NMAX]) {
+// clamp(theta + alpha d) joint by joint, read from the per-seed records in
+// shared memory (stride nt), so a line-search trial point is never
+// materialised as a register array (K19: register pressure at high DoF)
+template <class T>
+struct TrialTheta {
+    const DevRobotT<T>& rb;
+    const T* th;   // &S.th[owner], stride nt
+    const T* d;    // &S.dir[(kind * NMAX) * nt + owner], stride nt
+    int nt;
+    T alpha;
+    __device__ __forceinline__ T operator[](int j) const {
+        return clampf(th[j * nt] + alpha * d[j * nt], rb.j[j].lo, rb.j[j].hi);
+    }
+};
+
+template <int NMAX, bool EXACT = false, int REV = 0, class T, class A>
+__device__ __forceinline__ ResidT<T> eval_at(const DevRobotT<T>& rb, const TargetT<T>& tg, const A& th) {
     vec3<T> P[NMAX], Z[NMAX];   // unused (FRAMES = false), eliminated
     vec3<T> pe;
     QuatT<T> qe;
@@ -102,11 +117,16 @@ __device__ __forceinline__ ResidT<T> eval_at(const DevRobotT<T>& rb, const Targe
 // ---- LM direction (Eq. 12 via push-through, K4): A = W G W + lambda I,
 //      G_ik = sum_j J_ij J_kj / D_j; y = A^-1 W rho; dth_j = -(sum_i J_ij W_i y_i) / D_j,
 //      then the element-wise trust-region clamp (Alg. 4 l.6, R21)
-template <int NMAX, bool EXACT = false, class T>
+//      RECOMP (high DoF, K19): 1 / D_j recomputed from the column where it is
+//      used instead of held in NMAX registers (invD is then not read)
+template <int NMAX, bool EXACT = false, bool RECOMP = false, class T>
 __device__ __forceinline__ bool lm_direction(const DevRobotT<T>& rb, const DevCfg& c, const vec3<T> (&Jp)[NMAX],
                                              const vec3<T> (&Jo)[NMAX], const T (&invD)[NMAX],
                                              const T (&W)[6], const T (&rho)[6], T (&dth)[NMAX]) {
     const int n = rb.n;
+    auto inv_d = [&](int j) {
+        return RECOMP ? rcp_nr(fmax(dot3(Jp[j], Jp[j]) + dot3(Jo[j], Jo[j]), T(c.d_floor))) : invD[j];
+    };
     // G = sum_j (J_j / D_j) J_j^T: scale each column once, then one FMA per term
     T A[21];
 #pragma unroll
@@ -115,9 +135,10 @@ __device__ __forceinline__ bool lm_direction(const DevRobotT<T>& rb, const DevCf
     for (int j = 0; j < NMAX; ++j) {
         if (EXACT || j < n) {
             const T col[6] = {Jp[j].x, Jp[j].y, Jp[j].z, Jo[j].x, Jo[j].y, Jo[j].z};
+            const T id = inv_d(j);
 #pragma unroll
             for (int i = 0; i < 6; ++i) {
-                const T ui = col[i] * invD[j];
+                const T ui = col[i] * id;
 #pragma unroll
                 for (int kk = 0; kk <= i; ++kk) A[i * (i + 1) / 2 + kk] += ui * col[kk];
             }
@@ -140,7 +161,7 @@ __device__ __forceinline__ bool lm_direction(const DevRobotT<T>& rb, const DevCf
         if (EXACT || j < n) {
             const T s = Jp[j].x * y[0] + Jp[j].y * y[1] + Jp[j].z * y[2] + Jo[j].x * y[3] +
                         Jo[j].y * y[4] + Jo[j].z * y[5];
-            dth[j] = clampf(-s * invD[j], -Rt, Rt);
+            dth[j] = clampf(-s * inv_d(j), -Rt, Rt);
         }
     }
     return true;

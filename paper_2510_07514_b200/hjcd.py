@@ -27,7 +27,7 @@ EXPORTS = [
     "hjcd_workspace_size_host", "hjcd_solve", "hjcd_solve_timed", "hjcd_solve_host", "hjcd_ccd",
     "hjcd_solve_batch", "hjcd_select_topn", "hjcd_mmd", "hjcd_workspace_size_f64", "hjcd_solve_f64",
     "hjcd_pjik_f64", "hjcd_pose_error_f64", "hjcd_fk", "hjcd_fk_sfu", "hjcd_poccd", "hjcd_poccd_trace",
-    "hjcd_select_replicate", "hjcd_pjik", "hjcd_pjik_trace", "hjcd_select_best", "hjcd_status_string",
+    "hjcd_select_replicate", "hjcd_pjik", "hjcd_pjik_trace", "hjcd_select_best", "hjcd_status_string", "hjcd_poccd_kernel",
     "hjcd_last_cuda_error", "hjcd_version",
 ]
 
@@ -98,6 +98,8 @@ def lib():
         L.hjcd_pjik_trace.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P, P]
         L.hjcd_select_best.argtypes = [P, P, P, i32, P, P, P, P, P, P, P, P]
         L.hjcd_status_string.restype = C.c_char_p
+        L.hjcd_poccd_kernel.argtypes = [P, P]
+        L.hjcd_poccd_kernel.restype = C.c_char_p
         L.hjcd_last_cuda_error.restype = C.c_char_p
         L.hjcd_version.restype = C.c_char_p
         _lib = L
@@ -579,6 +581,11 @@ def select_best(robot: Robot, cfg: hjcd_config, targets, theta, ep_all, eo_all, 
                                   _ptr(ep_all), _ptr(eo_all), _ptr(q), _ptr(pe), _ptr(oe),
                                   _ptr(st), _stream(stream)), "hjcd_select_best")
     return q, pe, oe, st
+
+
+def poccd_kernel(robot: Robot, cfg: hjcd_config) -> str:
+    """Name of the PO-CCD kernel hjcd_solve launches for this robot / config."""
+    return lib().hjcd_poccd_kernel(robot.handle, C.byref(cfg)).decode()
 
 
 def version() -> str:

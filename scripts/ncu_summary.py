@@ -149,11 +149,14 @@ def main():
         tot = sum(ops.values())
         if tops:
             # executed FP32 flops from the per-instruction predicated-on thread counts
-            fl = 2 * tops.get("FFMA", 0) + tops.get("FMUL", 0) + tops.get("FADD", 0)
+            # (packed pairs count twice: FFMA2 = 2 FMAs, FMUL2 / FADD2 = 2 operations)
+            fl = (2 * tops.get("FFMA", 0) + tops.get("FMUL", 0) + tops.get("FADD", 0) + 4 * tops.get("FFMA2", 0)
+                  + 2 * tops.get("FMUL2", 0) + 2 * tops.get("FADD2", 0))
             dur = d.get("gpu__time_duration.sum", ("", ""))
             dur_s = _num(dur[0]) * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(
                 dur[1], 1e-3) if _num(dur[0]) else None
-            lines += ["", f"Executed FP32 flops per launch (2 FFMA + FMUL + FADD, thread level): {fl:.4g}"]
+            lines += ["", f"Executed FP32 flops per launch (2 FFMA + FMUL + FADD + 4 FFMA2 + 2 FMUL2 + 2 FADD2, "
+                          f"thread level): {fl:.4g}"]
             if dur_s:
                 lines.append(f"Executed FP32 rate: {fl / dur_s / 1e12:.2f} TFLOP/s at the captured duration")
                 traffic.setdefault("_executed_fp32_flops", {}).setdefault(config, {})[base] = fl

@@ -773,7 +773,7 @@ def test_solve_f64_high_dof(hjcd_lib, cuda):
     pe64, oe64 = fp64_errors(ch, N(q), tg)
     assert np.abs(pe64 - N(pe)).max() < 1e-10 and success(pe64, oe64).all()
     with pytest.raises(hjcd_lib.HjcdError):
-        hjcd_lib.solve_f64(rb, T(tg, cuda), hjcd_lib.config_from_params(params(M=256, K=16, B=192)))
+        hjcd_lib.solve_f64(rb, T(tg, cuda), hjcd_lib.config_from_params(params(M=256, K=16, B=256)))
 
 
 def test_concurrent_solves_on_two_streams(hjcd_lib, cuda):
