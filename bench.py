@@ -237,7 +237,18 @@ def relaunch(args_gpus):
     sk.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args_gpus}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
-    return subprocess.call(cmd)
+    return subprocess.call(cmd, env=nccl_log_env())
+
+
+def nccl_log_env():
+    """NCCL's communicator log (init, transports, NVLS) into a file per rank,
+    so the one stdout JSON line stays clean."""
+    env = dict(os.environ)
+    if "NCCL_DEBUG" not in env:
+        d = os.path.join(ROOT, "gpurun_out") if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "/tmp"
+        env.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,COLL",
+                   NCCL_DEBUG_FILE=os.path.join(d, "nccl.%h.%p.log"))
+    return env
 
 
 def launch_check(args):
@@ -333,6 +344,9 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         if backend == "nccl":
+            for k, v in nccl_log_env().items():   # before the communicator exists
+                if k.startswith("NCCL_DEBUG"):
+                    os.environ.setdefault(k, v)
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)

@@ -68,7 +68,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
     __shared__ T s_alpha[32];   // line-search steps beta^-a, a = 0..A (A <= 31), by repeated products
     const int nt = blockDim.x;
     const CoopSmem<T> S = coop_smem<T, NMAX>(coop_raw, nt);
-    constexpr bool SPEC_DIRS = NMAX >= 16 && sizeof(T) == 4;   // K19
+    constexpr bool SPEC_DIRS = NMAX >= 16 || sizeof(T) == 8;   // K19
     const int n = rb.n;
     const int used = c.copies * c.K;
     const int t = blockIdx.x;
