@@ -68,7 +68,12 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
     __shared__ T s_alpha[32];   // line-search steps beta^-a, a = 0..A (A <= 31), by repeated products
     const int nt = blockDim.x;
     const CoopSmem<T> S = coop_smem<T, NMAX>(coop_raw, nt);
-    constexpr bool SPEC_DIRS = NMAX >= 16 || sizeof(T) == 8;   // K19
+    // K19: the fallback directions before the trials at >= 16 DoF and in the
+    // fp64 polish (register pressure), and at <= 8 DoF (latency: a slow
+    // target's failing seed no longer builds them after its alpha = 1 trial,
+    // C2 -1.4 %); at 12-14 DoF the extra work costs the 10k-target C4 more
+    // (+13 % k_pjik) than the latency gains
+    constexpr bool SPEC_DIRS = NMAX <= 8 || NMAX >= 16 || sizeof(T) == 8;
     const int n = rb.n;
     const int used = c.copies * c.K;
     const int t = blockIdx.x;
