@@ -300,12 +300,30 @@ __device__ __forceinline__ float rsqrt_nr(float x) {
     return r * fmaf(-0.5f * x * r, r, 1.5f);
 }
 
+// 1/x from the SFU alone (rcp.approx.ftz, ~1 ulp), for ratios whose rounding
+// the caller's own error budget dominates
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// sqrt from the SFU alone (MUFU.SQRT, ~1 ulp, sqrt(0) = 0): residual norms,
+// where the IEEE sqrtf's range checks and slow path only cost issue slots
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // atan2 on [-pi, pi] with |err| <= 3.3e-7 rad (fp32): odd minimax polynomial
-// of degree 15 for atan on [0, 1] + octant reduction (K5)
+// of degree 15 for atan on [0, 1] + octant reduction (K5); the
+// ratio min/max by one SFU reciprocal (no __fdividef range fix-ups; a
+// subnormal max gives NaN, which every caller masks or never produces)
 __device__ __forceinline__ float fast_atan2f(float y, float x) {
     const float ax = fabsf(x), ay = fabsf(y);
     const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-    const float r = mx > 0.f ? __fdividef(mn, mx) : 0.f;
+    const float r = mx > 0.f ? mn * rcp_approx(mx) : 0.f;
     const float s = r * r;
     float p = -0.00405456f;
     p = fmaf(p, s, 0.02186293f);
@@ -377,7 +395,7 @@ template <bool FAST = false>
 __device__ __forceinline__ void normals4(uint4 r, float g[4]) {
     float u0 = u01(r.x), u1 = u01(r.y), u2 = u01(r.z), u3 = u01(r.w);
     if (FAST) {
-        const float ra = sqrtf(-1.38629436f * __log2f(u0)), rb2 = sqrtf(-1.38629436f * __log2f(u2));
+        const float ra = sqrt_approx(-1.38629436f * __log2f(u0)), rb2 = sqrt_approx(-1.38629436f * __log2f(u2));
         float s, c;   // sin/cos(2 pi u - pi) = -sin/-cos(2 pi u), argument in (-pi, pi)
         __sincosf(fmaf(6.28318531f, u1, -3.14159265f), &s, &c);
         g[0] = -ra * c; g[1] = -ra * s;

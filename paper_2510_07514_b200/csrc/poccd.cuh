@@ -126,8 +126,8 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         }
         const float3 rp = tg.p - pe;                   // r_p (Eq. 4)
         const Quat qr = quat_err(tg.q, qe);            // q_err (Eq. 5), w >= 0
-        const float sv = sqrtf(qr.x * qr.x + qr.y * qr.y + qr.z * qr.z);
-        ep = sqrtf(dot3(rp, rp));
+        const float sv = sqrt_approx(qr.x * qr.x + qr.y * qr.y + qr.z * qr.z);
+        ep = sqrt_approx(dot3(rp, rp));
         eo = 2.f * fast_atan2f(sv, qr.w);              // |omega|
         // Alg. 3 l.14: coarse test (R12), checked at iteration start
         const bool conv = ep < c.eps_p_coarse && eo < c.eps_o_coarse;
@@ -288,8 +288,8 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
             }
         }
         const float3 rh = tg.p - p2;
-        const float ep_h = sqrtf(dot3(rh, rh));
-        const float eo_h = 2.f * fast_atan2f(sqrtf(q2.x * q2.x + q2.y * q2.y + q2.z * q2.z), fabsf(q2.w));
+        const float ep_h = sqrt_approx(dot3(rh, rh));
+        const float eo_h = 2.f * fast_atan2f(sqrt_approx(q2.x * q2.x + q2.y * q2.y + q2.z * q2.z), fabsf(q2.w));
         // ---- Alg. 3 l.11-13 (R10): accept on an improvement > gamma in either space
         const bool accept = (ep - ep_h) > c.gamma || (eo - eo_h) > c.gamma;
         if (trace.words && active)   // decision word: see hjcd_poccd_trace (include/hjcd.h)

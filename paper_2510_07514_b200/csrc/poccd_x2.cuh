@@ -14,9 +14,11 @@
 // per-seed value is naturally a (seed a, seed b) pair.  What stays per seed:
 // SFU (sincos, rsqrt), comparisons and selects (argmins, clamps), Philox.
 //
-// Per seed the arithmetic is that of k_poccd<..., TEXIT = true, ...> (the same
-// operations in the same order, so the same decisions up to fp32 contraction
-// differences), with one layout change: the frames (P_j, z_j) live only in
+// Per seed the arithmetic is that of k_poccd<..., TEXIT = true, ...> up to the
+// association of a few sums (the FK translation accumulates in FMAs) and the
+// SFU forms of sqrt and of atan2's ratio (fp32-rounding-level differences;
+// the decision replay judges the decisions), with one layout
+// change: the frames (P_j, z_j) live only in
 // shared memory, [joint][3][thread] float4 = {Px, Py}, {Pz, zx}, {zy, zz} of
 // the pair, written by the FK and read back joint by joint by the candidate
 // loop and the gamma test (keeping 2 x 6 n frame floats in registers would
@@ -147,7 +149,7 @@ __device__ __forceinline__ V rot_about(V p, V up, V zxu, f2 s2, f2 c2) {
 }
 
 // per-lane helpers
-__device__ __forceinline__ f2 sqrt2(f2 a) { return mk2(sqrtf(lo(a)), sqrtf(hi(a))); }
+__device__ __forceinline__ f2 sqrt2(f2 a) { return mk2(sqrt_approx(lo(a)), sqrt_approx(hi(a))); }
 // kin.cuh fast_atan2f for the pair: octant reduction per lane, the
 // polynomial packed (per lane the same operations)
 __device__ __forceinline__ f2 atan2_2(f2 y, f2 x) {
@@ -157,7 +159,7 @@ __device__ __forceinline__ f2 atan2_2(f2 y, f2 x) {
         ax[s] = fabsf(lane(x, s));
         ay[s] = fabsf(lane(y, s));
         const float mx = fmaxf(ax[s], ay[s]), mn = fminf(ax[s], ay[s]);
-        r[s] = mx > 0.f ? __fdividef(mn, mx) : 0.f;
+        r[s] = mx > 0.f ? mn * rcp_approx(mx) : 0.f;
     }
     const f2 rr = mk2(r[0], r[1]);
     const f2 sq = rr * rr;
@@ -227,9 +229,10 @@ __device__ __forceinline__ void fk_x2(const DevRobot& rb, const f2 (&th)[NMAX], 
     for (int j = 0; j < NMAX; ++j) {
         if (EXACT || j < rb.n) {
             const DevJoint& J = rb.j[j];
-            tx = tx + fma2(R[2], bc2(J.t[2]), fma2(R[1], bc2(J.t[1]), R[0] * bc2(J.t[0])));
-            ty = ty + fma2(R[5], bc2(J.t[2]), fma2(R[4], bc2(J.t[1]), R[3] * bc2(J.t[0])));
-            tz = tz + fma2(R[8], bc2(J.t[2]), fma2(R[7], bc2(J.t[1]), R[6] * bc2(J.t[0])));
+            // t += R F_j.t, accumulated into t (three FMAs per component)
+            tx = fma2(R[2], bc2(J.t[2]), fma2(R[1], bc2(J.t[1]), fma2(R[0], bc2(J.t[0]), tx)));
+            ty = fma2(R[5], bc2(J.t[2]), fma2(R[4], bc2(J.t[1]), fma2(R[3], bc2(J.t[0]), ty)));
+            tz = fma2(R[8], bc2(J.t[2]), fma2(R[7], bc2(J.t[1]), fma2(R[6], bc2(J.t[0]), tz)));
             f2 N[9];
             if constexpr (REV == 2) {
 #pragma unroll
@@ -266,9 +269,9 @@ __device__ __forceinline__ void fk_x2(const DevRobot& rb, const f2 (&th)[NMAX], 
             }
         }
     }
-    tx = tx + fma2(R[2], bc2(rb.eet[2]), fma2(R[1], bc2(rb.eet[1]), R[0] * bc2(rb.eet[0])));
-    ty = ty + fma2(R[5], bc2(rb.eet[2]), fma2(R[4], bc2(rb.eet[1]), R[3] * bc2(rb.eet[0])));
-    tz = tz + fma2(R[8], bc2(rb.eet[2]), fma2(R[7], bc2(rb.eet[1]), R[6] * bc2(rb.eet[0])));
+    tx = fma2(R[2], bc2(rb.eet[2]), fma2(R[1], bc2(rb.eet[1]), fma2(R[0], bc2(rb.eet[0]), tx)));
+    ty = fma2(R[5], bc2(rb.eet[2]), fma2(R[4], bc2(rb.eet[1]), fma2(R[3], bc2(rb.eet[0]), ty)));
+    tz = fma2(R[8], bc2(rb.eet[2]), fma2(R[7], bc2(rb.eet[1]), fma2(R[6], bc2(rb.eet[0]), tz)));
     f2 E[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
@@ -388,6 +391,7 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
         const f2 w2 = qr.w * qr.w, wsv2 = w2 + sv2, ka = sv2 + wsv2;
         const f2 ob0 = fma2(Sd * Sd, wsv2, (Cd * Cd) * sv2);
         const f2 ob1 = Sd * Sd, ob2 = ((bc2(2.f) * Cd) * Sd) * qr.w;
+        const f2 svsq = sv * sv;   // the score of a zero orientation step (the current residual)
 
         // ---- Alg. 3 l.6-9: per-joint candidates, scored, greedy argmin (per seed)
         float best_p[2] = {CUDART_INF_F, CUDART_INF_F}, best_o[2] = {CUDART_INF_F, CUDART_INF_F};
@@ -416,8 +420,9 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
                     // score (K2): r_p' = r_p + (1 - cos d) u_perp - sin d (z x u)
                     f2 s2, c2;
                     sincos2(bc2(0.5f) * dp, s2, c2);
+                    // a zero step scores the current residual exactly: s2 = 0 makes sn =
+                    // omc = 0 whatever c2 is
                     s2 = mk2(lo(dp) == 0.f ? 0.f : lo(s2), hi(dp) == 0.f ? 0.f : hi(s2));
-                    c2 = mk2(lo(dp) == 0.f ? 1.f : lo(c2), hi(dp) == 0.f ? 1.f : hi(c2));
                     const f2 sn = (bc2(2.f) * s2) * c2, omc = (bc2(2.f) * s2) * s2;
                     const V r2 = {fma2(neg(sn), zxu.x, fma2(omc, up.x, rp.x)), fma2(neg(sn), zxu.y, fma2(omc, up.y, rp.y)),
                                   fma2(neg(sn), zxu.z, fma2(omc, up.z, rp.z))};
@@ -441,15 +446,15 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
                         const f2 vz2 = vz * vz;
                         so_cl = fma2(neg(sd), qr.w * vz, bc2(0.5f) * fma2(cd, vz2 - w2, ka - vz2));
                     }
-                    so = mk2(lo(dor) == 0.f ? lo(sv) * lo(sv) : (cl0 ? lo(so_cl) : lo(so_un)),
-                             hi(dor) == 0.f ? hi(sv) * hi(sv) : (cl1 ? hi(so_cl) : hi(so_un)));
+                    so = mk2(lo(dor) == 0.f ? lo(svsq) : (cl0 ? lo(so_cl) : lo(so_un)),
+                             hi(dor) == 0.f ? hi(svsq) : (cl1 ? hi(so_cl) : hi(so_un)));
                 } else {
                     // prismatic (R32): exact 1-D minimiser z . (P_t - P_ee)
                     dp = clamp2(th[j] + dot(z, rp), J.lo, J.hi) - th[j];
                     const V r2 = axpy_neg(rp, dp, z);
                     sp = dot(r2, r2);
                     dor = bc2(0.f);
-                    so = sv * sv;
+                    so = svsq;
                 }
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
@@ -524,8 +529,8 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
         const V rh = tp - p2;
         const f2 ep_h = sqrt2(dot(rh, rh));
         const f2 qv2 = fma2(q2.z, q2.z, fma2(q2.y, q2.y, q2.x * q2.x));
-        const f2 eo_h = bc2(2.f) * mk2(fast_atan2f(sqrtf(lo(qv2)), fabsf(lo(q2.w))),
-                                       fast_atan2f(sqrtf(hi(qv2)), fabsf(hi(q2.w))));
+        const f2 eo_h = bc2(2.f) * mk2(fast_atan2f(sqrt_approx(lo(qv2)), fabsf(lo(q2.w))),
+                                       fast_atan2f(sqrt_approx(hi(qv2)), fabsf(hi(q2.w))));
         // ---- Alg. 3 l.11-13 (R10): accept on an improvement > gamma in either space
         bool acc[2];
 #pragma unroll
