@@ -191,26 +191,28 @@ __device__ __forceinline__ void sincos2(f2 a, f2& s, f2& c) {
 }
 __device__ __forceinline__ f2 clamp2(f2 x, float l, float h) { return mk2(clampf(lo(x), l, h), clampf(hi(x), l, h)); }
 
-// frames in shared memory: [joint][3][nt] float4 {Px_a, Px_b, Py_a, Py_b},
-// {Pz_a, Pz_b, zx_a, zx_b}, {zy_a, zy_b, zz_a, zz_b}
-__device__ __forceinline__ void store_frame(float4* s, int j, int nt, V P, V Z) {
-    float4* p = s + (3 * j) * nt + threadIdx.x;
+// frames in shared memory: [joint][3][FR] float4 {Px_a, Px_b, Py_a, Py_b},
+// {Pz_a, Pz_b, zx_a, zx_b}, {zy_a, zy_b, zz_a, zz_b}; the stride is the
+// compile-time maximum CTA size, so every offset is an immediate
+constexpr int FR = 128;
+__device__ __forceinline__ void store_frame(float4* s, int j, V P, V Z) {
+    float4* p = s + (3 * j) * FR + threadIdx.x;
     p[0] = make_float4(lo(P.x), hi(P.x), lo(P.y), hi(P.y));
-    p[nt] = make_float4(lo(P.z), hi(P.z), lo(Z.x), hi(Z.x));
-    p[2 * nt] = make_float4(lo(Z.y), hi(Z.y), lo(Z.z), hi(Z.z));
+    p[FR] = make_float4(lo(P.z), hi(P.z), lo(Z.x), hi(Z.x));
+    p[2 * FR] = make_float4(lo(Z.y), hi(Z.y), lo(Z.z), hi(Z.z));
 }
-__device__ __forceinline__ void load_frame(const float4* s, int j, int nt, V& P, V& Z) {
-    const float4* p = s + (3 * j) * nt + threadIdx.x;
-    const float4 a = p[0], b = p[nt], c = p[2 * nt];
+__device__ __forceinline__ void load_frame(const float4* s, int j, V& P, V& Z) {
+    const float4* p = s + (3 * j) * FR + threadIdx.x;
+    const float4 a = p[0], b = p[FR], c = p[2 * FR];
     P = {mk2(a.x, a.y), mk2(a.z, a.w), mk2(b.x, b.y)};
     Z = {mk2(b.z, b.w), mk2(c.x, c.y), mk2(c.z, c.w)};
 }
 // joint ja of lane 0 and joint jb of lane 1 (the winners differ per seed)
-__device__ __forceinline__ void load_frame_lanes(const float4* s, int j0, int j1, int nt, V& P, V& Z) {
-    const float4* p0 = s + (3 * j0) * nt + threadIdx.x;
-    const float4* p1 = s + (3 * j1) * nt + threadIdx.x;
-    const float4 a0 = p0[0], b0 = p0[nt], c0 = p0[2 * nt];
-    const float4 a1 = p1[0], b1 = p1[nt], c1 = p1[2 * nt];
+__device__ __forceinline__ void load_frame_lanes(const float4* s, int j0, int j1, V& P, V& Z) {
+    const float4* p0 = s + (3 * j0) * FR + threadIdx.x;
+    const float4* p1 = s + (3 * j1) * FR + threadIdx.x;
+    const float4 a0 = p0[0], b0 = p0[FR], c0 = p0[2 * FR];
+    const float4 a1 = p1[0], b1 = p1[FR], c1 = p1[2 * FR];
     P = {mk2(a0.x, a1.y), mk2(a0.z, a1.w), mk2(b0.x, b1.y)};
     Z = {mk2(b0.z, b1.w), mk2(c0.x, c1.y), mk2(c0.z, c1.w)};
 }
@@ -220,7 +222,7 @@ __device__ __forceinline__ void load_frame_lanes(const float4* s, int j0, int j1
 // FK of the pair (Eq. 1; kin.cuh fk, general or REV = 2 DH-twist form), frames
 // to shared memory; returns the end-effector position and orientation
 template <int NMAX, bool EXACT, int REV>
-__device__ __forceinline__ void fk_x2(const DevRobot& rb, const f2 (&th)[NMAX], float4* s_fr, int nt,
+__device__ __forceinline__ void fk_x2(const DevRobot& rb, const f2 (&th)[NMAX], float4* s_fr,
                                       px::V& pe, px::Q& qe) {
     using namespace px;
     f2 R[9] = {bc2(1.f), bc2(0.f), bc2(0.f), bc2(0.f), bc2(1.f), bc2(0.f), bc2(0.f), bc2(0.f), bc2(1.f)};
@@ -249,7 +251,7 @@ __device__ __forceinline__ void fk_x2(const DevRobot& rb, const f2 (&th)[NMAX], 
                         N[3 * r + cc] = fma2(R[3 * r + 2], bc2(J.R[6 + cc]),
                                              fma2(R[3 * r + 1], bc2(J.R[3 + cc]), R[3 * r] * bc2(J.R[cc])));
             }
-            store_frame(s_fr, j, nt, V{tx, ty, tz}, V{N[2], N[5], N[8]});
+            store_frame(s_fr, j, V{tx, ty, tz}, V{N[2], N[5], N[8]});
             if (REV || J.type == HJCD_REVOLUTE) {
                 f2 s, c;
                 sincos2(th[j], s, c);   // K5: SFU sines in the coarse stage
@@ -300,7 +302,7 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
     const int n = rb.n;
     const int nt = (int)blockDim.x;
     __shared__ int s_flag[3];
-    extern __shared__ float4 s_fr[];   // [NMAX][3][nt] frames of the pair
+    extern __shared__ float4 s_fr[];   // [NMAX][3][FR] frames of the pair
     const int t = (int)(blockIdx.x / (unsigned)CL);
     const int m0 = 2 * ((int)(blockIdx.x - (unsigned)t * CL) * nt + (int)threadIdx.x);
     const bool act[2] = {m0 < M, m0 + 1 < M};
@@ -356,7 +358,7 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
                 }
             }
         }
-        fk_x2<NMAX, EXACT, REV>(rb, th, s_fr, nt, pe, qe);
+        fk_x2<NMAX, EXACT, REV>(rb, th, s_fr, pe, qe);
         const V rp = tp - pe;                        // r_p (Eq. 4)
         const Q qr = quat_err2(tg.q, qe);             // q_err (Eq. 5), w >= 0
         const f2 sv2 = fma2(qr.z, qr.z, fma2(qr.y, qr.y, qr.x * qr.x));
@@ -402,7 +404,7 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
             if (EXACT || j < n) {
                 const DevJoint& J = rb.j[j];
                 V Pj, z;
-                load_frame(s_fr, j, nt, Pj, z);
+                load_frame(s_fr, j, Pj, z);
                 f2 dp, sp, dor, so;
                 if (REV || J.type == HJCD_REVOLUTE) {
                     // Eqs. 8-9 (R3): signed angle between the projections of
@@ -486,7 +488,7 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
         Q q2 = qr;
         {
             V Pb, Zb;
-            load_frame_lanes(s_fr, jb[0], jb[1], nt, Pb, Zb);
+            load_frame_lanes(s_fr, jb[0], jb[1], Pb, Zb);
             const bool rb0 = REV || !((rb.pmask >> jb[0]) & 1u), rb1 = REV || !((rb.pmask >> jb[1]) & 1u);
             const f2 dbb = mk2(db[0], db[1]);
             f2 s2, c2;
@@ -506,7 +508,7 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
         }
         if (__any_sync(0xffffffffu, ja[0] >= 0 || ja[1] >= 0)) {
             V Pa, Za;
-            load_frame_lanes(s_fr, ja[0] >= 0 ? ja[0] : 0, ja[1] >= 0 ? ja[1] : 0, nt, Pa, Za);
+            load_frame_lanes(s_fr, ja[0] >= 0 ? ja[0] : 0, ja[1] >= 0 ? ja[1] : 0, Pa, Za);
             const bool ra0 = REV || (ja[0] >= 0 && !((rb.pmask >> ja[0]) & 1u));
             const bool ra1 = REV || (ja[1] >= 0 && !((rb.pmask >> ja[1]) & 1u));
             const f2 daa = mk2(da[0], da[1]);   // 0 where there is no second joint: identity
@@ -578,7 +580,7 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
                     float g[4];
                     normals4<true>(draw(c, tid, (uint32_t)(m0 + 2 * (ol - lane_id) + sl), P_PERTURB, (uint32_t)k,
                                         (uint32_t)blk), g);
-                    s_fr[(2 * blk + sl) * nt + (threadIdx.x - lane_id + ol)] = make_float4(g[0], g[1], g[2], g[3]);
+                    s_fr[(2 * blk + sl) * FR + (threadIdx.x - lane_id + ol)] = make_float4(g[0], g[1], g[2], g[3]);
                 }
                 __syncwarp();
 #pragma unroll
@@ -587,7 +589,7 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
 #pragma unroll
                         for (int blk = 0; blk < NB; ++blk) {
                             if (EXACT || 4 * blk < n) {
-                                const float4 g4 = s_fr[(2 * blk + sl) * nt + threadIdx.x];
+                                const float4 g4 = s_fr[(2 * blk + sl) * FR + threadIdx.x];
                                 const float g[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
                                 for (int e = 0; e < 4; ++e) {
@@ -636,11 +638,11 @@ static cudaError_t launch_poccd_x2_r(const DevRobot& rb, const DevCfg& c, const 
     int nt, CL;
     texit_shape_x2(c.M, nt, CL);
     if (CL > 16) return cudaErrorInvalidConfiguration;
-    const size_t smem = (size_t)NMAX * 3 * nt * sizeof(float4);
+    const size_t smem = (size_t)NMAX * 3 * px::FR * sizeof(float4);
     static std::atomic<unsigned long long> attr{0};
     cudaError_t e = once_per_device(attr, [] {
         cudaError_t e2 = cudaFuncSetAttribute(k_poccd_x2<NMAX, EXACT, REV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)((size_t)NMAX * 3 * 128 * sizeof(float4)));
+                                              (int)((size_t)NMAX * 3 * px::FR * sizeof(float4)));
         if (e2 == cudaSuccess)
             e2 = cudaFuncSetAttribute(k_poccd_x2<NMAX, EXACT, REV>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         return e2;
