@@ -53,6 +53,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
     // the frames (P_j, z_j) of this iteration, per thread, so the two moved
     // joints' frames are two indexed loads instead of 2 x NMAX predicated selects
     constexpr bool FRAMES_SMEM = NMAX <= HJCD_FRAMES_SMEM_MAX;
+    constexpr int FRS = poccd_cta(NMAX);   // frame stride: the largest CTA size (immediate offsets, K20b)
     extern __shared__ float4 s_frames[];   // [NMAX][blockDim] (P.xyz, z.x), then float2 [NMAX][blockDim] (z.yz)
     if (TEXIT) {
         t = (int)(blockIdx.x / (unsigned)CL);
@@ -115,12 +116,12 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         }
         fk<NMAX, true, EXACT, true, REV>(rb, th, P, Z, pe, qe);
         if constexpr (FRAMES_SMEM) {
-            float2* s_fz = (float2*)(s_frames + NMAX * blockDim.x);
+            float2* s_fz = (float2*)(s_frames + NMAX * FRS);
 #pragma unroll
             for (int j = 0; j < NMAX; ++j) {
                 if (EXACT || j < n) {
-                    s_frames[j * blockDim.x + threadIdx.x] = make_float4(P[j].x, P[j].y, P[j].z, Z[j].x);
-                    s_fz[j * blockDim.x + threadIdx.x] = make_float2(Z[j].y, Z[j].z);
+                    s_frames[j * FRS + threadIdx.x] = make_float4(P[j].x, P[j].y, P[j].z, Z[j].x);
+                    s_fz[j * FRS + threadIdx.x] = make_float2(Z[j].y, Z[j].z);
                 }
             }
         }
@@ -241,13 +242,13 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
         const int ta = (!REV && ja >= 0 && ((rb.pmask >> ja) & 1u)) ? HJCD_PRISMATIC : HJCD_REVOLUTE;
         const int tb = (!REV && ((rb.pmask >> jb) & 1u)) ? HJCD_PRISMATIC : HJCD_REVOLUTE;
         if constexpr (FRAMES_SMEM) {
-            const float2* s_fz = (const float2*)(s_frames + NMAX * blockDim.x);
-            const float4 fb = s_frames[jb * blockDim.x + threadIdx.x];
-            const float2 gb = s_fz[jb * blockDim.x + threadIdx.x];
+            const float2* s_fz = (const float2*)(s_frames + NMAX * FRS);
+            const float4 fb = s_frames[jb * FRS + threadIdx.x];
+            const float2 gb = s_fz[jb * FRS + threadIdx.x];
             Pb = f3(fb.x, fb.y, fb.z); Zb = f3(fb.w, gb.x, gb.y);
             if (ja >= 0) {
-                const float4 fa = s_frames[ja * blockDim.x + threadIdx.x];
-                const float2 ga = s_fz[ja * blockDim.x + threadIdx.x];
+                const float4 fa = s_frames[ja * FRS + threadIdx.x];
+                const float2 ga = s_fz[ja * FRS + threadIdx.x];
                 Pa = f3(fa.x, fa.y, fa.z); Za = f3(fa.w, ga.x, ga.y);
             }
         } else {
@@ -324,14 +325,14 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
                     const int ol = (int)__fns(rej, 0u, r + 1);
                     float g[4];
                     normals4<true>(draw(c, tid, (uint32_t)(m - lane + ol), P_PERTURB, (uint32_t)k, (uint32_t)blk), g);
-                    s_frames[blk * blockDim.x + (threadIdx.x - lane + ol)] = make_float4(g[0], g[1], g[2], g[3]);
+                    s_frames[blk * FRS + (threadIdx.x - lane + ol)] = make_float4(g[0], g[1], g[2], g[3]);
                 }
                 __syncwarp();
                 if (active && !accept) {
 #pragma unroll
                     for (int blk = 0; blk < (NMAX + 3) / 4; ++blk) {
                         if (EXACT || 4 * blk < n) {
-                            const float4 g4 = s_frames[blk * blockDim.x + threadIdx.x];
+                            const float4 g4 = s_frames[blk * FRS + threadIdx.x];
                             const float g[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
                             for (int e = 0; e < 4; ++e) {
@@ -369,8 +370,8 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
 }
 
 template <int NMAX>
-inline size_t poccd_smem(int nt) {   // the per-thread frames (24 B per joint)
-    return NMAX <= HJCD_FRAMES_SMEM_MAX ? (size_t)NMAX * nt * (sizeof(float4) + sizeof(float2)) : 0;
+inline size_t poccd_smem(int) {   // the per-thread frames (24 B per joint), stride poccd_cta(NMAX)
+    return NMAX <= HJCD_FRAMES_SMEM_MAX ? (size_t)NMAX * poccd_cta(NMAX) * (sizeof(float4) + sizeof(float2)) : 0;
 }
 
 template <int NMAX, bool EXACT, int REV>
