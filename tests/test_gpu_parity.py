@@ -109,6 +109,8 @@ def test_poccd_per_seed_parity(hjcd_lib, cuda, name, iters, floor):
     tg, _ = targets_for(ch, 4)
     agree, clean, ref, _ = poccd_compare(hjcd_lib, cuda, ch, p, tg)
     bad = clean & ~agree
+    print(f"\n{name} iters={iters}: per-seed agreement {agree.mean():.4f} (floor {floor}), clean seeds "
+          f"{clean.mean():.4f}, clean agreeing {agree[clean].mean() if clean.any() else 1.0:.4f}")
     assert not bad.any(), f"{bad.sum()} clean seeds disagree (margins {ref['margin'][bad][:5]})"
     assert agree.mean() >= floor, agree.mean()
 
@@ -321,6 +323,8 @@ def test_pjik_per_seed_parity(hjcd_lib, cuda, name, sigma, iters, floor):
     seeds = inputs.near_configs(ch, np.repeat(th0[:, None, :], B, 1), sigma, seed=8).astype(np.float32)
     agree, clean, ref, out = pjik_compare(hjcd_lib, cuda, ch, p, tg, seeds)
     bad = clean & ~agree
+    print(f"\n{name} sigma={sigma} iters={iters}: per-seed agreement {agree.mean():.4f} (floor {floor}), clean "
+          f"seeds {clean.mean():.4f}")
     assert not bad.any(), f"{bad.sum()} clean seeds disagree"
     assert agree.mean() >= floor, agree.mean()
 
