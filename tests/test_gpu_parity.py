@@ -100,9 +100,12 @@ def poccd_compare(hjcd_lib, cuda, ch, p, tg, seeds=None):
     return agree, clean, ref, out
 
 
+# floors ~5 points under the measured agreement (profiles/r02n_perseed.log:
+# Panda 1.0 at 1-64 iterations, Fetch 0.98 / 0.94, 14-DoF 0.96); every clean
+# seed must agree regardless, and the decision replay covers every seed
 @pytest.mark.parametrize("name,iters,floor", [
-    ("panda", 1, 0.95), ("panda", 4, 0.9), ("panda", 16, 0.7), ("panda", 64, 0.2),
-    ("fetch", 4, 0.85), ("fetch", 64, 0.1), ("panda_x14", 16, 0.5)])
+    ("panda", 1, 0.95), ("panda", 4, 0.95), ("panda", 16, 0.95), ("panda", 64, 0.95),
+    ("fetch", 4, 0.93), ("fetch", 64, 0.89), ("panda_x14", 16, 0.91)])
 def test_poccd_per_seed_parity(hjcd_lib, cuda, name, iters, floor):
     ch = inputs.robot(name)
     p = params(M=300, ccd_iters=iters, ccd_early_exit=0)
@@ -313,8 +316,8 @@ def pjik_compare(hjcd_lib, cuda, ch, p, tg, seeds):
 
 
 @pytest.mark.parametrize("name,sigma,iters,floor", [
-    ("panda", 0.02, 32, 0.9), ("panda", 0.3, 32, 0.6), ("fetch", 0.1, 32, 0.6),
-    ("panda_x14", 0.05, 16, 0.6), ("panda", 0.3, 128, 0.5)])
+    ("panda", 0.02, 32, 0.95), ("panda", 0.3, 32, 0.94), ("fetch", 0.1, 32, 0.95),
+    ("panda_x14", 0.05, 16, 0.95), ("panda", 0.3, 128, 0.94)])
 def test_pjik_per_seed_parity(hjcd_lib, cuda, name, sigma, iters, floor):
     ch = inputs.robot(name)
     Tn, B = 6, 40
