@@ -74,6 +74,13 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
     // C2 -1.4 %); at 12-14 DoF the extra work costs the 10k-target C4 more
     // (+13 % k_pjik) than the latency gains
     constexpr bool SPEC_DIRS = NMAX <= 8 || NMAX >= 16 || sizeof(T) == 8;
+    // K21: at <= 8 DoF in fp32 the three directions form one straight-line
+    // block (branch-free Cholesky and dogleg, unconditional records), so the
+    // two 6x6 solves interleave
+#ifndef HJCD_NB_DIRS
+#define HJCD_NB_DIRS 1
+#endif
+    constexpr bool NBD = HJCD_NB_DIRS && SPEC_DIRS && NMAX <= 8 && sizeof(T) == 4;
     const int n = rb.n;
     const int used = c.copies * c.K;
     const int t = blockIdx.x;
@@ -212,7 +219,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                 for (int i = 0; i < 6; ++i) W[i] = T(i < 3 ? c.w_p : c.w_o) * rcp_nr(T(1) + sqrt(rn[i]));
             }
             c0 = cost_w(W, r.rho);
-            have_lm = lm_direction<NMAX, EXACT, SPEC_DIRS>(rb, c, Jp, Jo, invD, W, r.rho, dth);
+            have_lm = lm_direction<NMAX, EXACT, SPEC_DIRS, NBD>(rb, c, Jp, Jo, invD, W, r.rho, dth);
             // theta and the LM direction into this seed's record: the alpha = 1
             // trial reads them from there (K19), and so does the cooperative
             // cascade if that trial fails
@@ -227,15 +234,25 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                 // registers: no spills at 18 / 24 DoF); seeds whose alpha = 1
                 // trial then succeeds did this work in vain
                 flags = have_lm ? 1 : 0;
-                if (dogleg_direction<NMAX, EXACT>(rb, c, Jp, Jo, r.rho, dth, tt)) {   // Eqs. 14-15
-                    flags |= 2;
+                if constexpr (NBD) {
+                    // records written whatever the flags say: holes are skipped by flags
+                    if (dogleg_direction<NMAX, EXACT, true>(rb, c, Jp, Jo, r.rho, dth, tt)) flags |= 2;   // Eqs. 14-15
 #pragma unroll
                     for (int j = 0; j < NMAX; ++j) S.dir[(1 * NMAX + j) * nt + b] = dth[j];
-                }
-                if (single_coord_direction<NMAX, EXACT>(rb, c, Jp, Jo, W, r.rho, dth, ist)) {   // Eq. 16
-                    flags |= 4;
+                    if (single_coord_direction<NMAX, EXACT>(rb, c, Jp, Jo, W, r.rho, dth, ist)) flags |= 4;   // Eq. 16
 #pragma unroll
                     for (int j = 0; j < NMAX; ++j) S.dir[(2 * NMAX + j) * nt + b] = dth[j];
+                } else {
+                    if (dogleg_direction<NMAX, EXACT>(rb, c, Jp, Jo, r.rho, dth, tt)) {   // Eqs. 14-15
+                        flags |= 2;
+#pragma unroll
+                        for (int j = 0; j < NMAX; ++j) S.dir[(1 * NMAX + j) * nt + b] = dth[j];
+                    }
+                    if (single_coord_direction<NMAX, EXACT>(rb, c, Jp, Jo, W, r.rho, dth, ist)) {   // Eq. 16
+                        flags |= 4;
+#pragma unroll
+                        for (int j = 0; j < NMAX; ++j) S.dir[(2 * NMAX + j) * nt + b] = dth[j];
+                    }
                 }
                 // theta back from its record: not held in registers across the directions
 #pragma unroll

@@ -18,10 +18,13 @@ __device__ __forceinline__ double atan2_r(double y, double x) { return atan2(y, 
 // 6x6 SPD solve by Cholesky, packed lower triangle A[i*(i+1)/2 + j]; the
 // pivots are kept as reciprocals (rsqrt + Newton in fp32), so the
 // factorisation and both substitutions are multiply-only.  Returns false if a
-// pivot is not positive.
-template <class T>
+// pivot is not positive.  NB (K21): no early exit -- the solve runs to the
+// end on any input and the flag alone says whether b is valid, so the code
+// is one straight-line block
+template <class T, bool NB = false>
 __device__ __forceinline__ bool chol6_solve(T (&A)[21], T (&b)[6]) {
     T id[6];
+    bool ok = true;
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
 #pragma unroll
@@ -30,7 +33,8 @@ __device__ __forceinline__ bool chol6_solve(T (&A)[21], T (&b)[6]) {
 #pragma unroll
             for (int k = 0; k < j; ++k) s -= A[i * (i + 1) / 2 + k] * A[j * (j + 1) / 2 + k];
             if (i == j) {
-                if (!(s > T(1e-30))) return false;
+                if constexpr (NB) ok = ok && (s > T(1e-30));
+                else if (!(s > T(1e-30))) return false;
                 id[i] = rsqrt_nr(s);
                 A[i * (i + 1) / 2 + i] = s * id[i];
             } else {
@@ -52,7 +56,7 @@ __device__ __forceinline__ bool chol6_solve(T (&A)[21], T (&b)[6]) {
         for (int k = i + 1; k < 6; ++k) s -= A[k * (k + 1) / 2 + i] * b[k];
         b[i] = s * id[i];
     }
-    return true;
+    return ok;
 }
 
 template <class V>
@@ -119,7 +123,7 @@ __device__ __forceinline__ ResidT<T> eval_at(const DevRobotT<T>& rb, const Targe
 //      then the element-wise trust-region clamp (Alg. 4 l.6, R21)
 //      RECOMP (high DoF, K19): 1 / D_j recomputed from the column where it is
 //      used instead of held in NMAX registers (invD is then not read)
-template <int NMAX, bool EXACT = false, bool RECOMP = false, class T>
+template <int NMAX, bool EXACT = false, bool RECOMP = false, bool NB = false, class T>
 __device__ __forceinline__ bool lm_direction(const DevRobotT<T>& rb, const DevCfg& c, const vec3<T> (&Jp)[NMAX],
                                              const vec3<T> (&Jo)[NMAX], const T (&invD)[NMAX],
                                              const T (&W)[6], const T (&rho)[6], T (&dth)[NMAX]) {
@@ -152,7 +156,9 @@ __device__ __forceinline__ bool lm_direction(const DevRobotT<T>& rb, const DevCf
     T y[6];
 #pragma unroll
     for (int i = 0; i < 6; ++i) y[i] = W[i] * rho[i];
-    if (!chol6_solve(A, y)) return false;
+    bool ok = true;
+    if constexpr (NB) ok = chol6_solve<T, true>(A, y);
+    else if (!chol6_solve(A, y)) return false;
 #pragma unroll
     for (int i = 0; i < 6; ++i) y[i] *= W[i];
     const T Rt = T(c.R);
@@ -164,12 +170,14 @@ __device__ __forceinline__ bool lm_direction(const DevRobotT<T>& rb, const DevCf
             dth[j] = clampf(-s * inv_d(j), -Rt, Rt);
         }
     }
-    return true;
+    return ok;
 }
 
 // ---- dogleg direction (Eqs. 14-15, R23): GD = -alpha_c J^T rho (Cauchy),
 //      GN = -J^T (J J^T + d_floor I)^-1 rho, smallest tau in [0,1] with |dth(tau)| <= R
-template <int NMAX, bool EXACT = false, class T>
+//      NB (K21, fp32): branch-free -- the degenerate cases are a flag, the
+//      divisions and square roots are SFU reciprocals / rsqrt + Newton
+template <int NMAX, bool EXACT = false, bool NB = false, class T>
 __device__ __forceinline__ bool dogleg_direction(const DevRobotT<T>& rb, const DevCfg& c, const vec3<T> (&Jp)[NMAX],
                                                  const vec3<T> (&Jo)[NMAX], const T (&rho)[6],
                                                  T (&dth)[NMAX], T (&gn)[NMAX]) {
@@ -192,8 +200,10 @@ __device__ __forceinline__ bool dogleg_direction(const DevRobotT<T>& rb, const D
             if (EXACT || j < n) s += jrow(Jp[j], Jo[j], i) * dth[j];
         jg2 += s * s;
     }
-    if (!(gg > T(0)) || !(jg2 > T(0))) return false;
-    const T alpha_c = gg / jg2;
+    bool ok = (gg > T(0)) && (jg2 > T(0));
+    if constexpr (!NB)
+        if (!ok) return false;
+    const T alpha_c = NB ? gg * rcp_nr(jg2) : gg / jg2;
     T A[21];
 #pragma unroll
     for (int i = 0; i < 6; ++i)
@@ -208,7 +218,8 @@ __device__ __forceinline__ bool dogleg_direction(const DevRobotT<T>& rb, const D
     T y[6];
 #pragma unroll
     for (int i = 0; i < 6; ++i) y[i] = rho[i];
-    if (!chol6_solve(A, y)) return false;
+    if constexpr (NB) ok = chol6_solve<T, true>(A, y) && ok;
+    else if (!chol6_solve(A, y)) return false;
     T ngn2 = T(0), ngd2 = T(0);
 #pragma unroll
     for (int j = 0; j < NMAX; ++j) {
@@ -223,7 +234,26 @@ __device__ __forceinline__ bool dogleg_direction(const DevRobotT<T>& rb, const D
     const T Rt = T(c.R);
     const T R2 = Rt * Rt;
     T wgd, wgn;   // step = wgd * GD + wgn * GN
-    if (ngn2 <= R2) {
+    if constexpr (NB) {
+        T qa = T(0), qb = T(0);
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) {
+            if (EXACT || j < n) {
+                const T d = dth[j] - gn[j];
+                qa += d * d;
+                qb += T(2) * gn[j] * d;
+            }
+        }
+        const T qc = ngn2 - R2;
+        const T disc = qb * qb - T(4) * qa * qc;
+        const T sd = disc > T(0) ? disc * rsqrt_nr(disc) : T(0);
+        const T tau = (qa > T(0) && disc >= T(0))
+                          ? ((qb < T(0)) ? (T(2) * qc) * rcp_nr(-qb + sd) : (-qb - sd) * rcp_nr(T(2) * qa))
+                          : T(-1);
+        const bool inside = ngn2 <= R2, blend = tau >= T(0) && tau <= T(1);
+        wgd = inside ? T(0) : blend ? tau : Rt * rsqrt_nr(ngd2);
+        wgn = inside ? T(1) : blend ? T(1) - tau : T(0);
+    } else if (ngn2 <= R2) {
         wgd = T(0); wgn = T(1);
     } else {
         T qa = T(0), qb = T(0);
@@ -248,7 +278,7 @@ __device__ __forceinline__ bool dogleg_direction(const DevRobotT<T>& rb, const D
 #pragma unroll
     for (int j = 0; j < NMAX; ++j)
         if (EXACT || j < n) dth[j] = wgd * dth[j] + wgn * gn[j];
-    return true;
+    return ok;
 }
 
 // ---- single-coordinate direction (Eq. 16, R24): i* = argmax |g_i|, g = J^T W^2 rho,
@@ -273,12 +303,11 @@ __device__ __forceinline__ bool single_coord_direction(const DevRobotT<T>& rb, c
         }
     }
     ist_out = ist;
-    if (gbest == T(0)) return false;
     const T Rt = T(c.R);
     const T step = (gbest > T(0)) ? -fmin(gabs, Rt) : fmin(gabs, Rt);
 #pragma unroll
     for (int j = 0; j < NMAX; ++j) dth[j] = (j == ist) ? step : T(0);
-    return true;
+    return gbest != T(0);
 }
 
 // cascade position q < 2A + 2 of a seed -> (direction kind, alpha index):
