@@ -291,6 +291,8 @@ struct Layout {
     size_t theta1, cost1, seeds2, ep2, eo2, ready, total;
 };
 
+constexpr int kOrderMaxTargets = 2048;
+
 Layout layout(int dof, long long T, const hjcd_config* c) {
     Layout L;
     size_t off = 0;
@@ -299,9 +301,11 @@ Layout layout(int dof, long long T, const hjcd_config* c) {
     L.seeds2 = off; off += align256((size_t)T * c->B * dof * sizeof(float));
     L.ep2 = off;    off += align256((size_t)T * c->B * sizeof(float));
     L.eo2 = off;    off += align256((size_t)T * c->B * sizeof(float));
-    L.ready = off;  off += align256((size_t)T * sizeof(uint32_t));   // K10 per-target PO-CCD completion counts
+    // K10 per-target PO-CCD completion counts [T], then the K26 polish-order
+    // stacks (next [T], heads [kReadyBuckets], pushed, popped)
+    L.ready = off;  off += align256((size_t)((2 * T + kReadyWords + 63) & ~63) * sizeof(uint32_t));
 #ifdef HJCD_PROBE
-    off += align256((size_t)((T + 63) & ~63) * 4 + 5 * (size_t)T * 8);
+    off += align256(5 * (size_t)T * 8);
 #endif
     L.total = off;
     return L;
@@ -344,14 +348,24 @@ cudaError_t solve_linked(const hjcd_robot* r, const DevCfg& d, const float* targ
     link.spin_limit = (1ull << 26) * (unsigned long long)(1 + d.ccd_iters / 64);
     link.Mpad = 2;
     while (link.Mpad < d.M) link.Mpad <<= 1;
+    // K26: the stop-iteration order pays where the slowest polish targets set
+    // the step, a batch of a few polish waves (C2 -1 to -2.5 %, 300 targets
+    // -9 %, 2000 -4 %); with every polish CTA resident at once (<= 2 per SM)
+    // the order is moot and the pops only add traffic (100 targets +12 %),
+    // and 10k-target batches contend on the stack heads (+6-10 %):
+    // profiles/r02t_k26_polish_order_ab.log
+    int dev = 0, nsm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    link.order = (T > 2 * nsm && T <= kOrderMaxTargets) ? 1 : 0;
 #ifdef HJCD_PROBE
-    g_probe = (unsigned long long*)(link.ready + ((T + 63) & ~63));
+    g_probe = (unsigned long long*)(link.ready + ((2 * T + kReadyWords + 63) & ~63));
     g_probe_T = T;
     if ((e = cudaMemsetAsync(g_probe, 0xff, (size_t)T * 8, s)) != cudaSuccess ||
         (e = cudaMemsetAsync(g_probe + T, 0, 4 * (size_t)T * 8, s)) != cudaSuccess)
         return e;
 #endif
-    if ((e = cudaMemsetAsync(link.ready, 0, (size_t)T * sizeof(uint32_t), s)) != cudaSuccess ||
+    if ((e = cudaMemsetAsync(link.ready, 0, (size_t)(2 * T + kReadyWords) * sizeof(uint32_t), s)) != cudaSuccess ||
         (e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s, TraceOut(),
                           link.ready)) != cudaSuccess ||
         (e = launch_pjik(r->dev, d, targets, T, nullptr, seeds2, ep2, eo2, nullptr, nullptr, s, link)) != cudaSuccess)

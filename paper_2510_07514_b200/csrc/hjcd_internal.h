@@ -75,6 +75,8 @@ struct StageLink {
     // readiness polls (~0.5 us apart) before a waiting PJ-IK CTA traps instead
     // of hanging (a stage 1 that cannot complete); scaled with the PO-CCD budget
     unsigned long long spin_limit = 0;
+    // K26: pop the targets in PO-CCD stop-iteration order (else blockIdx order)
+    int32_t order = 0;
     // not part of the link: PJ-IK decision words [T][B][lm_iters] and theta at
     // the start of every iteration [T][B][lm_iters + 1][n], or nullptr
     // (hjcd_pjik_trace; word format in include/hjcd.h), for any launch
@@ -101,6 +103,69 @@ inline void texit_shape_x2(int M, int& nt, int& CL) {
     CL = (pairs + nt - 1) / nt;
 }
 
+// DESIGN K26: the polish order.  hjcd_solve's PO-CCD clusters push each
+// finished target onto one of kReadyBuckets lock-free stacks, keyed by its
+// stop iteration k* (R12b), and every PJ-IK CTA pops the target of the
+// smallest k* that is ready: the targets whose polish runs longest are the
+// ones whose stage 1 stopped earliest (scripts/slow_predict.py), so they start
+// first instead of wherever their index puts them in the polish grid.  Only
+// the schedule changes (each target's arithmetic depends on its index alone).
+// Layout after ready[T]: next[T] (stack links, t + 1; 0 = end), head[buckets]
+// (t + 1 of the top; 0 = empty); all zeroed with ready.  Each target is pushed
+// once and popped once, so the stacks have no ABA problem.
+constexpr int kReadyBuckets = 64;
+constexpr int kReadyWords = kReadyBuckets + 2;   // + pushed, popped counts
+
+__device__ __forceinline__ void ready_push(uint32_t* ready, int T, int t, int kstar) {
+    uint32_t* nxt = ready + T;
+    uint32_t* head = ready + 2 * T + (kstar < kReadyBuckets - 1 ? kstar : kReadyBuckets - 1);
+    __threadfence();   // the cluster's seeds (fenced by every CTA before its count) before the link
+    uint32_t h = *(volatile uint32_t*)head;
+    for (;;) {
+        *(volatile uint32_t*)(nxt + t) = h;
+        __threadfence();
+        const uint32_t prev = atomicCAS(head, h, (uint32_t)t + 1u);
+        if (prev == h) break;
+        h = prev;
+    }
+    atomicAdd(ready + 2 * T + kReadyBuckets, 1u);   // pushed
+}
+
+// one warp: the lowest non-empty bucket's top, popped; -1 if every bucket is
+// empty right now.  The result is warp-uniform.
+__device__ __forceinline__ int ready_pop_warp(uint32_t* ready, int T) {
+    uint32_t* nxt = ready + T;
+    uint32_t* head = ready + 2 * T;
+    const int lane = (int)(threadIdx.x & 31);
+    for (;;) {
+        // one word polled while nothing is queued (the heads only when a pop can succeed)
+        const uint32_t pushed = *(volatile uint32_t*)(head + kReadyBuckets);
+        const uint32_t popped = *(volatile uint32_t*)(head + kReadyBuckets + 1);
+        if (pushed == popped) return -1;
+        const uint32_t h0 = *(volatile uint32_t*)(head + lane);
+        const uint32_t h1 = *(volatile uint32_t*)(head + 32 + lane);
+        const unsigned m0 = __ballot_sync(0xffffffffu, h0 != 0u), m1 = __ballot_sync(0xffffffffu, h1 != 0u);
+        if (!(m0 | m1)) return -1;
+        const int b = m0 ? __ffs(m0) - 1 : 32 + __ffs(m1) - 1;
+        int got = -2;   // -2: lost a race, rescan
+        if (lane == (b & 31)) {
+            uint32_t h = b < 32 ? h0 : h1;
+            while (h != 0u) {
+                const uint32_t nx = *(volatile uint32_t*)(nxt + (h - 1u));
+                const uint32_t prev = atomicCAS(head + b, h, nx);
+                if (prev == h) { got = (int)(h - 1u); break; }
+                h = prev;
+            }
+        }
+        if (got >= 0) atomicAdd(head + kReadyBuckets + 1, 1u);   // popped
+        got = __shfl_sync(0xffffffffu, got, b & 31);
+        if (got >= 0) {
+            __threadfence();
+            return got;
+        }
+    }
+}
+
 #ifdef HJCD_PROBE
 // A/B diagnostic build only: %globaltimer stamps of the K10 schedule, stored
 // after the readiness counts: [5][T] = PO-CCD first CTA start, last CTA end,
@@ -111,7 +176,7 @@ __device__ __forceinline__ unsigned long long probe_now() {
     return v;
 }
 __device__ __forceinline__ unsigned long long* probe_base(uint32_t* ready, int T) {
-    return (unsigned long long*)(ready + ((T + 63) & ~63));
+    return (unsigned long long*)(ready + ((2 * T + kReadyWords + 63) & ~63));   // after the K26 queue
 }
 #endif
 

@@ -81,10 +81,34 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
 #define HJCD_NB_DIRS 1
 #endif
     constexpr bool NBD = HJCD_NB_DIRS && SPEC_DIRS && NMAX <= 8 && sizeof(T) == 4;
+#ifndef HJCD_POLISH_ORDER
+#define HJCD_POLISH_ORDER 1
+#endif
     const int n = rb.n;
     const int used = c.copies * c.K;
-    const int t = blockIdx.x;
+    int t = blockIdx.x;
     const int b = threadIdx.x;
+#if HJCD_POLISH_ORDER
+    if (link.ready && link.order) {
+        // DESIGN K26: this CTA polishes the ready target of the smallest
+        // PO-CCD stop iteration, not target blockIdx.x (every PO-CCD CTA is
+        // resident or done when this grid starts, and each pushes its target,
+        // so the wait is bounded; a stage 1 that cannot complete traps)
+        __shared__ int s_t;
+        if (b < 32) {
+            int got = -1;
+            for (unsigned long long spins = 0;; ++spins) {
+                got = ready_pop_warp(link.ready, (int)gridDim.x);
+                if (got >= 0) break;
+                if (spins > link.spin_limit) __trap();
+                __nanosleep(500);
+            }
+            if (b == 0) s_t = got;
+        }
+        __syncthreads();
+        t = s_t;
+    }
+#endif
     const int lane = b & 31;
     const bool active = b < used;
     const TargetT<T> tg = load_target<T>(targets + 7ll * t);

@@ -627,7 +627,8 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
     if (ready) {   // DESIGN K10: this CTA's seeds of target t are in memory
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) atomicAdd(ready + t, 1u);
+        if (threadIdx.x == 0 && atomicAdd(ready + t, 1u) + 1u == (uint32_t)CL)
+            ready_push(ready, T, t, k);   // DESIGN K26: the cluster's last CTA queues the target
     }
 }
 
