@@ -2,6 +2,7 @@
 // canonicalisation (fp64), config validation, workspace carving and the
 // stream-ordered launch sequence of hjcd_solve (Alg. 2).
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -291,7 +292,7 @@ struct Layout {
     size_t theta1, cost1, seeds2, ep2, eo2, ready, total;
 };
 
-constexpr int kOrderMaxTargets = 2048;
+constexpr int kOrderMaxTargets = 5000;   // (A/B: HJCD_ORDER_MAX)
 
 Layout layout(int dof, long long T, const hjcd_config* c) {
     Layout L;
@@ -302,7 +303,7 @@ Layout layout(int dof, long long T, const hjcd_config* c) {
     L.ep2 = off;    off += align256((size_t)T * c->B * sizeof(float));
     L.eo2 = off;    off += align256((size_t)T * c->B * sizeof(float));
     // K10 per-target PO-CCD completion counts [T], then the K26 polish-order
-    // stacks (next [T], heads [kReadyBuckets], pushed, popped)
+    // stacks (next [T], heads [shards][buckets], pushed, popped)
     L.ready = off;  off += align256((size_t)((2 * T + kReadyWords + 63) & ~63) * sizeof(uint32_t));
 #ifdef HJCD_PROBE
     off += align256(5 * (size_t)T * 8);
@@ -348,16 +349,21 @@ cudaError_t solve_linked(const hjcd_robot* r, const DevCfg& d, const float* targ
     link.spin_limit = (1ull << 26) * (unsigned long long)(1 + d.ccd_iters / 64);
     link.Mpad = 2;
     while (link.Mpad < d.M) link.Mpad <<= 1;
-    // K26: the stop-iteration order pays where the slowest polish targets set
-    // the step, a batch of a few polish waves (C2 -1 to -2.5 %, 300 targets
-    // -9 %, 2000 -4 %); with every polish CTA resident at once (<= 2 per SM)
-    // the order is moot and the pops only add traffic (100 targets +12 %),
-    // and 10k-target batches contend on the stack heads (+6-10 %):
-    // profiles/r02t_k26_polish_order_ab.log
+    // K26: the stop-iteration order (C2 -2 %, 300 targets -9 %, 2000 -8 %,
+    // 4000 -6 %); with every polish CTA resident at once (<= 2 per SM) the
+    // order is moot and the pops only add traffic (100 targets +12 %); from
+    // ~10k targets the tail is amortised and the claims cost about what the
+    // order gains (Panda -1 %, Fetch-like 0, 14-DoF +1 %), so those run in
+    // target order.  The sharded stacks (K30) keep the claims free of
+    // contention: profiles/r02t_k26_polish_order_ab.log, r02y_*
     int dev = 0, nsm = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaGetLastError();
-    link.order = (T > 2 * nsm && T <= kOrderMaxTargets) ? 1 : 0;
+    static const int order_max = [] {   // A/B override of the K26 batch bound
+        const char* v = std::getenv("HJCD_ORDER_MAX");
+        return v ? std::atoi(v) : kOrderMaxTargets;
+    }();
+    link.order = (T > 2 * nsm && T <= order_max) ? 1 : 0;
 #ifdef HJCD_PROBE
     g_probe = (unsigned long long*)(link.ready + ((2 * T + kReadyWords + 63) & ~63));
     g_probe_T = T;

@@ -104,21 +104,31 @@ inline void texit_shape_x2(int M, int& nt, int& CL) {
 }
 
 // DESIGN K26: the polish order.  hjcd_solve's PO-CCD clusters push each
-// finished target onto one of kReadyBuckets lock-free stacks, keyed by its
-// stop iteration k* (R12b), and every PJ-IK CTA pops the target of the
-// smallest k* that is ready: the targets whose polish runs longest are the
-// ones whose stage 1 stopped earliest (scripts/slow_predict.py), so they start
-// first instead of wherever their index puts them in the polish grid.  Only
-// the schedule changes (each target's arithmetic depends on its index alone).
-// Layout after ready[T]: next[T] (stack links, t + 1; 0 = end), head[buckets]
-// (t + 1 of the top; 0 = empty); all zeroed with ready.  Each target is pushed
-// once and popped once, so the stacks have no ABA problem.
+// finished target onto a lock-free stack keyed by its stop iteration k*
+// (R12b), and every PJ-IK CTA pops the ready target of the smallest k*: the
+// targets whose polish runs longest are the ones whose stage 1 stopped
+// earliest (scripts/slow_predict.py), so they start first instead of wherever
+// their index puts them in the polish grid.  Only the schedule changes (each
+// target's arithmetic depends on its index alone).  K30: the stacks are
+// sharded (target t in shard t mod kReadyShards, a claiming CTA starts at
+// shard blockIdx mod kReadyShards), so concurrent claims rarely race on one
+// head; the order is then k*-first within a shard, and the shards drain at
+// the same rate.  Layout after ready[T]: next[T] (stack links, t + 1; 0 =
+// end), head[shards][buckets] (t + 1 of the top; 0 = empty), pushed, popped;
+// all zeroed with ready.  Each target is pushed once and popped once, so the
+// stacks have no ABA problem.
 constexpr int kReadyBuckets = 64;
-constexpr int kReadyWords = kReadyBuckets + 2;   // + pushed, popped counts
+#ifndef HJCD_READY_SHARDS
+#define HJCD_READY_SHARDS 16
+#endif
+constexpr int kReadyShards = HJCD_READY_SHARDS;
+constexpr int kReadyHeads = kReadyShards * kReadyBuckets;
+constexpr int kReadyWords = kReadyHeads + 2;   // + pushed, popped counts
 
 __device__ __forceinline__ void ready_push(uint32_t* ready, int T, int t, int kstar) {
     uint32_t* nxt = ready + T;
-    uint32_t* head = ready + 2 * T + (kstar < kReadyBuckets - 1 ? kstar : kReadyBuckets - 1);
+    uint32_t* head = ready + 2 * T + (t % kReadyShards) * kReadyBuckets +
+                     (kstar < kReadyBuckets - 1 ? kstar : kReadyBuckets - 1);
     __threadfence();   // the cluster's seeds (fenced by every CTA before its count) before the link
     uint32_t h = *(volatile uint32_t*)head;
     for (;;) {
@@ -128,26 +138,31 @@ __device__ __forceinline__ void ready_push(uint32_t* ready, int T, int t, int ks
         if (prev == h) break;
         h = prev;
     }
-    atomicAdd(ready + 2 * T + kReadyBuckets, 1u);   // pushed
+    atomicAdd(ready + 2 * T + kReadyHeads, 1u);   // pushed
 }
 
-// one warp: the lowest non-empty bucket's top, popped; -1 if every bucket is
-// empty right now.  The result is warp-uniform.
-__device__ __forceinline__ int ready_pop_warp(uint32_t* ready, int T) {
+// one warp: the lowest non-empty bucket's top in the first non-empty shard
+// from `shard0` on, popped; -1 if every stack is empty right now.  The result
+// is warp-uniform.
+__device__ __forceinline__ int ready_pop_warp(uint32_t* ready, int T, int shard0) {
     uint32_t* nxt = ready + T;
-    uint32_t* head = ready + 2 * T;
+    uint32_t* heads = ready + 2 * T;
     const int lane = (int)(threadIdx.x & 31);
-    for (;;) {
-        // one word polled while nothing is queued (the heads only when a pop can succeed)
-        const uint32_t pushed = *(volatile uint32_t*)(head + kReadyBuckets);
-        const uint32_t popped = *(volatile uint32_t*)(head + kReadyBuckets + 1);
-        if (pushed == popped) return -1;
+    // one word pair polled while nothing is queued (the heads only when a pop can succeed)
+    const uint32_t pushed = *(volatile uint32_t*)(heads + kReadyHeads);
+    const uint32_t popped = *(volatile uint32_t*)(heads + kReadyHeads + 1);
+    if (pushed == popped) return -1;
+    for (int sh = 0; sh < kReadyShards;) {
+        uint32_t* head = heads + ((shard0 + sh) % kReadyShards) * kReadyBuckets;
         const uint32_t h0 = *(volatile uint32_t*)(head + lane);
         const uint32_t h1 = *(volatile uint32_t*)(head + 32 + lane);
         const unsigned m0 = __ballot_sync(0xffffffffu, h0 != 0u), m1 = __ballot_sync(0xffffffffu, h1 != 0u);
-        if (!(m0 | m1)) return -1;
+        if (!(m0 | m1)) {   // this shard is empty: the next one
+            ++sh;
+            continue;
+        }
         const int b = m0 ? __ffs(m0) - 1 : 32 + __ffs(m1) - 1;
-        int got = -2;   // -2: lost a race, rescan
+        int got = -2;   // -2: lost a race, rescan this shard
         if (lane == (b & 31)) {
             uint32_t h = b < 32 ? h0 : h1;
             while (h != 0u) {
@@ -157,13 +172,14 @@ __device__ __forceinline__ int ready_pop_warp(uint32_t* ready, int T) {
                 h = prev;
             }
         }
-        if (got >= 0) atomicAdd(head + kReadyBuckets + 1, 1u);   // popped
+        if (got >= 0) atomicAdd(heads + kReadyHeads + 1, 1u);   // popped
         got = __shfl_sync(0xffffffffu, got, b & 31);
         if (got >= 0) {
             __threadfence();
             return got;
         }
     }
+    return -1;
 }
 
 #ifdef HJCD_PROBE

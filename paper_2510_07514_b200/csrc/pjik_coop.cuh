@@ -98,7 +98,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
         if (b < 32) {
             int got = -1;
             for (unsigned long long spins = 0;; ++spins) {
-                got = ready_pop_warp(link.ready, (int)gridDim.x);
+                got = ready_pop_warp(link.ready, (int)gridDim.x, (int)(blockIdx.x % kReadyShards));
                 if (got >= 0) break;
                 if (spins > link.spin_limit) __trap();
                 __nanosleep(500);

@@ -15,7 +15,7 @@ from paper_2510_07514_b200 import hjcd, inputs
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 CFG = {"c2": ("panda", 1000), "c3": ("fetch_like8", 10000), "c4": ("panda_x14", 10000),
-       "c2_T10000": ("panda", 10000), "c3_T1000": ("fetch_like8", 1000), "c2_T300": ("panda", 300), "c2_T2000": ("panda", 2000), "c2_T100": ("panda", 100),
+       "c2_T10000": ("panda", 10000), "c3_T1000": ("fetch_like8", 1000), "c2_T300": ("panda", 300), "c2_T2000": ("panda", 2000), "c2_T4000": ("panda", 4000), "c2_T100": ("panda", 100),
        "x12": ("panda_x12", 1000), "x18": ("panda_x18", 1000), "x24": ("panda_x24", 1000), "x13": ("panda_x13", 1000)}
 rname, T = CFG[cfgname]
 chain = inputs.robot(rname)
