@@ -17,6 +17,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef HJCD_VOTE_RELAXED
+#define HJCD_VOTE_RELAXED 1
+#endif
+
 namespace hjcd {
 
 // TEXIT = false: one thread per (target, seed) anywhere in the grid; each seed
@@ -139,12 +143,27 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
             cg::cluster_group cluster = cg::this_cluster();
             const int slot = k % 3;
             const unsigned vote = __ballot_sync(0xffffffffu, conv && active);
+#if HJCD_VOTE_RELAXED
+            // K31: one flag tagged with the iteration (k + 1 means "a seed
+            // passed at k"; nothing resets it: if any seed passed at k every
+            // CTA stops at k, so no later tag can overwrite it unread), written
+            // and fenced by the voting lanes only, then a RELAXED cluster
+            // arrive: the default release arrive fences every warp-iteration
+            (void)slot;
+            if (vote && (threadIdx.x & 31) == 0) {
+                for (int r = 0; r < CL; ++r) *cluster.map_shared_rank(&s_flag[0], r) = k + 1;
+                asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            }
+            asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+            if (*(volatile int*)&s_flag[0] == k + 1) break;
+#else
             if (vote && (threadIdx.x & 31) == 0)
                 for (int r = 0; r < CL; ++r) *cluster.map_shared_rank(&s_flag[slot], r) = 1;
             cluster.sync();
             const bool any = s_flag[slot] != 0;
             if (threadIdx.x == 0) s_flag[(k + 2) % 3] = 0;
             if (any) break;
+#endif
         } else if (conv) {
             break;
         }
