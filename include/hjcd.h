@@ -161,7 +161,8 @@ hjcd_status hjcd_workspace_size_host(const hjcd_robot* r, int32_t T, const hjcd_
  * kernel, PJ-IK as its programmatic dependent launch (it starts on each target
  * as soon as that target's stage 1 is in memory, K10; for
  * 2 x SMs < T <= 5000 its CTAs take the ready targets in order of their
- * PO-CCD stop iteration, smallest first, K26/K30) and the best select.  Results are
+ * PO-CCD stop iteration, smallest first, K26/K30) and the best select; for
+ * T >= 5000 at >= 12 DoF the staged sequence of hjcd_solve_timed (K33).  Results are
  * bitwise those of hjcd_solve_timed's staged sequence. */
 hjcd_status hjcd_solve(const hjcd_robot* r, const hjcd_config* c, const float* targets, int32_t T,
                        float* q_out, float* pos_err, float* ori_err, int32_t* status,

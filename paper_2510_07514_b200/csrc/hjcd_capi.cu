@@ -515,13 +515,18 @@ hjcd_status hjcd_solve_timed(const hjcd_robot* r, const hjcd_config* c, const fl
     auto mark = [&](int i) -> cudaError_t {
         return (events && events[i]) ? cudaEventRecord((cudaEvent_t)events[i], s) : cudaSuccess;
     };
-    if (!events) {   // DESIGN K10: PJ-IK as a dependent launch of PO-CCD
+    // K33: at >= 12 DoF and >= 5000 targets the staged sequence is faster than
+    // the dependent launch (C4: 35.9 vs 36.3 ms): the 14-DoF polish CTAs
+    // (255 registers) overlapping PO-CCD's last wave and doing the top-K
+    // themselves cost more than the separate top-K kernel
+    const bool staged = T >= 5000 && r->dof >= 12;
+    if (!events && !staged) {   // DESIGN K10: PJ-IK as a dependent launch of PO-CCD
         e = solve_linked(r, d, targets, T, L, ws, s, [&](const float* th, const float* ep, const float* eo) {
             return launch_select_best(r->dev, d, targets, T, th, ep, eo, q_out, pos_err, ori_err, status, s);
         });
         return e == cudaSuccess ? HJCD_OK : cuda_fail(e);
     }
-    // stage events requested: the staged sequence, one kernel per stage
+    // stage events requested (or K33): the staged sequence, one kernel per stage
     if ((e = mark(0)) != cudaSuccess) return cuda_fail(e);
     // Alg. 2 l.1: PO-CCD over M seeds per target
     if ((e = launch_poccd(r->dev, d, targets, T, nullptr, theta1, cost1, nullptr, nullptr, nullptr, s)) != cudaSuccess ||
