@@ -32,7 +32,10 @@ struct CoopSmem {
     T* n0;         // [nt]
     int* flags;    // [nt]  bit0 LM, bit1 dogleg, bit2 single
     unsigned char* own;    // [nt]  rank among the failing seeds -> owner slot
-    unsigned long long* ok;   // [nt]  success bits in cascade order
+    // [8][nt] u64: byte q of slot o's word q / 8 = cascade position q succeeded
+    // (K34: plain byte stores, word-major so each owner reads its words
+    // conflict-free; replaces one contended 64-bit atomicOr per success)
+    unsigned long long* ok;
 };
 
 template <class T, int NMAX>
@@ -40,7 +43,7 @@ __device__ __forceinline__ CoopSmem<T> coop_smem(void* base, int nt) {
     CoopSmem<T> s;
     unsigned long long* p64 = (unsigned long long*)base;
     s.ok = p64;
-    T* f = (T*)(p64 + nt);
+    T* f = (T*)(p64 + 8 * nt);
     s.th = f; f += NMAX * nt;
     s.dir = f; f += 3 * NMAX * nt;
     s.W = f; f += 6 * nt;
@@ -53,7 +56,7 @@ __device__ __forceinline__ CoopSmem<T> coop_smem(void* base, int nt) {
 
 template <class T, int NMAX>
 size_t coop_smem_bytes(int nt) {
-    return (size_t)nt * (8 + sizeof(T) * (4 * NMAX + 6 + 2) + 4 + 1);
+    return (size_t)nt * (64 + sizeof(T) * (4 * NMAX + 6 + 2) + 4 + 1);
 }
 
 // REV: every DoF joint is revolute (no per-joint type branches)
@@ -328,7 +331,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                 const unsigned fail = __ballot_sync(0xffffffffu, need);
                 int rank = __popc(fail & ((1u << lane) - 1u));
                 if (lane == 0) s_wtot[b >> 5] = __popc(fail);
-                S.ok[b] = 0ull;
+                for (int w = 0; w < (2 * c.A + 2 + 7) / 8; ++w) S.ok[w * nt + b] = 0ull;
                 __syncthreads();
                 P2MARK(3);
                 int nfail = 0;
@@ -380,7 +383,7 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
                 if (phase == 0) {
                     own_ok = ok;
                 } else if (ok) {
-                    atomicOr(&S.ok[o], 1ull << qq);
+                    ((unsigned char*)(S.ok + (qq >> 3) * nt + o))[qq & 7] = 1;
                 }
             }
             if (phase == 0) {
@@ -400,9 +403,12 @@ k_pjik_coop(const __grid_constant__ DevRobotT<T> rb, const __grid_constant__ Dev
             __syncthreads();
             P2MARK(5);
             if (need) {
-                const unsigned long long m = S.ok[b];
-                if (m) {
-                    const int qq = __ffsll((long long)m) - 1;   // first success in cascade order
+                int qq = -1;   // first success in cascade order
+                for (int w = 0; w < (2 * c.A + 2 + 7) / 8; ++w) {
+                    const unsigned long long m = S.ok[w * nt + b];
+                    if (qq < 0 && m) qq = 8 * w + (__ffsll((long long)m) - 1) / 8;
+                }
+                if (qq >= 0) {
                     int kind, a;
                     decode_item(qq, c.A, kind, a);
                     const T alpha = s_alpha[a];
