@@ -738,12 +738,17 @@ def test_solve_other_chains(hjcd_lib, cuda, name):
 
 
 @pytest.mark.parametrize("name,M,Tn,early", [("panda", 1000, 300, 1), ("fetch", 64, 50, 1),
-                                             ("panda_x24", 2000, 20, 1), ("panda", 256, 40, 0)])
+                                             ("panda_x24", 2000, 20, 1), ("panda", 256, 40, 0),
+                                             ("panda", 64, 297, 1), ("fetch", 64, 5001, 1),
+                                             ("panda_x14", 64, 5000, 1)])
 def test_solve_dependent_launch_equals_staged(hjcd_lib, cuda, name, M, Tn, early):
     """DESIGN K10: hjcd_solve without stage events launches PJ-IK as a dependent
     of PO-CCD (per-target readiness counts, top-K + replication in the PJ-IK
     prologue); with events it runs one kernel per stage. Both must give the
-    same bytes, and solve_batch must equal the staged entry points."""
+    same bytes, and solve_batch must equal the staged entry points.  The
+    batch sizes also cover the K26/K30 polish order (ordered for 2 x SMs < T
+    <= 5000: 297; unordered above: 5001) and K33 (>= 12 DoF, T >= 5000: the
+    staged sequence)."""
     import torch
     ch = inputs.robot(name)
     rb = hjcd_lib.Robot(ch)
