@@ -190,8 +190,12 @@ def main():
         lines.append("")
     with open(os.path.join(prof, f"{tag}_ncu.md"), "w") as f:
         f.write("\n".join(lines))
-    with open(tpath, "w") as f:
-        json.dump(traffic, f, indent=1, sort_keys=True)
+    # the traffic table is merged only for a bench capture (with its launch
+    # list) or when HJCD_CONFIG names the workload: a side capture (one slow
+    # target, another config) must not overwrite the bench's C2 numbers
+    if launches or "HJCD_CONFIG" in os.environ:
+        with open(tpath, "w") as f:
+            json.dump(traffic, f, indent=1, sort_keys=True)
     print("\n".join(lines))
 
 
