@@ -20,6 +20,9 @@ namespace cg = cooperative_groups;
 #ifndef HJCD_VOTE_RELAXED
 #define HJCD_VOTE_RELAXED 1
 #endif
+#ifndef HJCD_X1_UNIFORM
+#define HJCD_X1_UNIFORM 1
+#endif
 
 namespace hjcd {
 
@@ -219,6 +222,19 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
                     const float tsum = th[j] + (vz != 0.f ? copysignf(dphi, vz) : 0.f);
                     dor = clampf(tsum, J.lo, J.hi) - th[j];
                     // score (K2): |v'|^2 of q_err (x) q(z, -d), monotone in |omega'|
+#if HJCD_X1_UNIFORM
+                    {   // K40: the three cases computed branch-free and selected (no divergence)
+                        const float avz = fabsf(vz);
+                        const float so_un = ob0 - avz * fmaf(ob1, avz, ob2);   // K2b closed form
+                        // clamped step: the same closed form at the effective d, in
+                        // double angles: C^2 = (1 + cos d) / 2, S^2 = (1 - cos d) / 2, 2 C S = sin d
+                        float sd, cd;
+                        __sincosf(dor, &sd, &cd);
+                        const float vz2 = vz * vz;
+                        const float so_cl = 0.5f * fmaf(cd, vz2 - w2, ka - vz2) - sd * (qr.w * vz);
+                        so = dor == 0.f ? sv * sv : ((tsum >= J.lo && tsum <= J.hi) ? so_un : so_cl);
+                    }
+#else
                     if (dor == 0.f) {
                         so = sv * sv;                     // zero step: the current residual, exactly
                     } else if (tsum >= J.lo && tsum <= J.hi) {
@@ -231,6 +247,7 @@ k_poccd(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c,
                         const float vz2 = vz * vz;
                         so = 0.5f * fmaf(cd, vz2 - w2, ka - vz2) - sd * (qr.w * vz);
                     }
+#endif
                 } else {
                     // prismatic (R32): exact 1-D minimiser z . (P_t - P_ee)
                     dp = clampf(th[j] + dot3(z, rp), J.lo, J.hi) - th[j];

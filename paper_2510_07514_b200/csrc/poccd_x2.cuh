@@ -35,6 +35,10 @@ namespace cg = cooperative_groups;
 #ifndef HJCD_VOTE_RELAXED
 #define HJCD_VOTE_RELAXED 1
 #endif
+// K40 (A/B): the two warp-voted branches of the iteration taken unconditionally
+#ifndef HJCD_X2_UNIFORM
+#define HJCD_X2_UNIFORM 1
+#endif
 
 namespace hjcd {
 namespace px {
@@ -460,7 +464,7 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
                     const bool cl0 = !(lo(tsum) >= J.lo && lo(tsum) <= J.hi) && lo(dor) != 0.f;
                     const bool cl1 = !(hi(tsum) >= J.lo && hi(tsum) <= J.hi) && hi(dor) != 0.f;
                     f2 so_cl = so_un;
-                    if (__any_sync(0xffffffffu, cl0 || cl1)) {
+                    if (HJCD_X2_UNIFORM || __any_sync(0xffffffffu, cl0 || cl1)) {
                         // clamped step: the closed form at the effective d, in double angles
                         f2 sd, cd;
                         sincos2(dor, sd, cd);
@@ -525,7 +529,7 @@ k_poccd_x2(const __grid_constant__ DevRobot rb, const __grid_constant__ DevCfg c
                   mk2(rb0 ? lo(qrr.y) : lo(q2.y), rb1 ? hi(qrr.y) : hi(q2.y)),
                   mk2(rb0 ? lo(qrr.z) : lo(q2.z), rb1 ? hi(qrr.z) : hi(q2.z))};
         }
-        if (__any_sync(0xffffffffu, ja[0] >= 0 || ja[1] >= 0)) {
+        if (HJCD_X2_UNIFORM || __any_sync(0xffffffffu, ja[0] >= 0 || ja[1] >= 0)) {
             V Pa, Za;
             load_frame_lanes(s_fr, ja[0] >= 0 ? ja[0] : 0, ja[1] >= 0 ? ja[1] : 0, Pa, Za);
             const bool ra0 = REV || (ja[0] >= 0 && !((rb.pmask >> ja[0]) & 1u));
