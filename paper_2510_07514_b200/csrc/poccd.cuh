@@ -12,6 +12,7 @@
 // perturbation.  Seeding (Alg. 3 l.2-3) is fused in.  Per-seed freeze on the
 // coarse test (Alg. 3 l.14) is deterministic.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "kin.cuh"
 
@@ -453,13 +454,23 @@ static cudaError_t launch_poccd_r(const DevRobot& rb, const DevCfg& c, const flo
     cfg.blockDim = dim3(nt, 1, 1);
     cfg.dynamicSmemBytes = poccd_smem<NMAX>(nt);
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // K42: the 256-thread-CTA clusters (12 / 14 DoF, K15) with the
+    // load-balancing scheduling policy (C4 -2.9 %, 12 DoF -1.7 %; at 18 / 24
+    // DoF it costs 2.5-5 %, so those keep the default); A/B:
+    // HJCD_CLUSTER_POLICY (0 default, 1 spread, 2 load balancing)
+    static const int policy = [] {
+        const char* v = std::getenv("HJCD_CLUSTER_POLICY");
+        return v ? std::atoi(v) : (poccd_cta(NMAX) == 256 ? 2 : 0);
+    }();
+    attr[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    attr[1].val.clusterSchedulingPolicyPreference = (cudaClusterSchedulingPolicy)policy;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = policy ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, k_poccd<NMAX, EXACT, true, REV>, rb, c, targets, T, seeds, theta, cost, ep, eo,
                               iters, CL, trace, ready);
 }

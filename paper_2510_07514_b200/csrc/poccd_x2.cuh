@@ -27,6 +27,7 @@
 // Mapping: the M seeds of a target live in one thread-block cluster of CL CTAs
 // x nt threads; thread i of CTA rank r holds seeds m = 2 (r nt + i) and m + 1.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "kin.cuh"
 
@@ -679,13 +680,22 @@ static cudaError_t launch_poccd_x2_r(const DevRobot& rb, const DevCfg& c, const 
     cfg.blockDim = dim3(nt, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr1[1];
+    cudaLaunchAttribute attr1[2];
     attr1[0].id = cudaLaunchAttributeClusterDimension;
     attr1[0].val.clusterDim.x = CL;
     attr1[0].val.clusterDim.y = 1;
     attr1[0].val.clusterDim.z = 1;
+    // A/B (K42): the cluster scheduling policy (0 default, 1 spread, 2 load
+    // balancing); the default suits the dependent launch here (load balancing:
+    // PO-CCD alone -1 to -3 %, the C3 step +8 %)
+    static const int policy = [] {
+        const char* v = std::getenv("HJCD_X2_CLUSTER_POLICY");
+        return v ? std::atoi(v) : 0;
+    }();
+    attr1[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    attr1[1].val.clusterSchedulingPolicyPreference = (cudaClusterSchedulingPolicy)policy;
     cfg.attrs = attr1;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = policy ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, k_poccd_x2<NMAX, EXACT, REV>, rb, c, targets, T, theta, cost, ep, eo, iters, CL,
                               trace, ready);
 }
